@@ -1,0 +1,106 @@
+"""ctypes front end of the C oracle (jz_oracle.c). TEST INFRASTRUCTURE ONLY.
+
+Definition computed (PAPER.md L295/L432/L453-454): for each query
+row i the k smallest (d2, j) over all points j (self included, ties -> lower j),
+d2 the canonical FP32 formula  fmaf(dz,dz,fmaf(dy,dy,dx*dx)),  dx = RN(q-s)
+wrapped to the minimal image [-L/2, L/2) when a periodic box is given.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "jz_oracle.c")
+_BUILD = os.path.join(_HERE, "_build")
+_LIB = os.path.join(_BUILD, "libjzoracle.so")
+_lock = threading.Lock()
+_lib = None
+
+CFLAGS = ["-O2", "-fopenmp", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-std=c11"]
+
+
+def build_oracle(force: bool = False) -> str:
+    """Compile jz_oracle.c into oracle/_build/libjzoracle.so (if stale)."""
+    os.makedirs(_BUILD, exist_ok=True)
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def _load():
+    global _lib
+    with _lock:
+        if _lib is None:
+            lib = ctypes.CDLL(build_oracle())
+            P = ctypes.c_void_p
+            lib.oracle_knn_brute.argtypes = [P, ctypes.c_int64, P, ctypes.c_int, P, ctypes.c_int64, P, P, ctypes.c_int]
+            lib.oracle_knn_brute.restype = ctypes.c_int
+            lib.oracle_knn_grid.argtypes = [P, ctypes.c_int64, P, ctypes.c_int, P, ctypes.c_int64, P, P,
+                                            ctypes.c_int, ctypes.c_double]
+            lib.oracle_knn_grid.restype = ctypes.c_int
+            lib.oracle_pair_d2.argtypes = [P, P, ctypes.c_int64, P, P]
+            lib.oracle_pair_d2.restype = None
+            lib.oracle_max_threads.argtypes = []
+            lib.oracle_max_threads.restype = ctypes.c_int
+            _lib = lib
+    return _lib
+
+
+def oracle_threads() -> int:
+    return int(_load().oracle_max_threads())
+
+
+def _prep(pos, box):
+    pos = np.ascontiguousarray(pos, dtype=np.float32)
+    if pos.ndim != 2 or pos.shape[1] != 3:
+        raise ValueError("pos must be [n,3]")
+    b = None
+    if box is not None:
+        b = np.ascontiguousarray(np.broadcast_to(np.asarray(box, dtype=np.float32), (3,)))
+    return pos, b
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data
+
+
+def _run(fn, pos, k, box, rows, threads, *extra):
+    pos, b = _prep(pos, box)
+    n = pos.shape[0]
+    if rows is None:
+        nrows, r = n, None
+    else:
+        r = np.ascontiguousarray(rows, dtype=np.int64)
+        nrows = r.shape[0]
+    idx = np.empty((nrows, k), dtype=np.int32)
+    d2 = np.empty((nrows, k), dtype=np.float32)
+    rc = fn(_ptr(pos), n, _ptr(b), int(k), _ptr(r), nrows, _ptr(idx), _ptr(d2), int(threads or 0), *extra)
+    if rc != 0:
+        raise ValueError(f"oracle returned status {rc} (n={n}, k={k})")
+    return idx, d2
+
+
+def knn_brute(pos, k: int, box=None, rows=None, threads: int | None = None):
+    """O(N^2) definition. Returns (idx int32 [m,k], d2 float32 [m,k])."""
+    return _run(_load().oracle_knn_brute, pos, k, box, rows, threads)
+
+
+def knn_grid(pos, k: int, box=None, rows=None, threads: int | None = None, per_cell: float = 2.0):
+    """Uniform-grid shell search, same bits as knn_brute."""
+    return _run(_load().oracle_knn_grid, pos, k, box, rows, threads, ctypes.c_double(per_cell))
+
+
+def pair_d2(a, b, box=None):
+    """Canonical FP32 d2 for explicit pairs a[i], b[i]."""
+    a, bx = _prep(a, box)
+    b = np.ascontiguousarray(b, dtype=np.float32)
+    out = np.empty(a.shape[0], dtype=np.float32)
+    _load().oracle_pair_d2(_ptr(a), _ptr(b), a.shape[0], _ptr(bx), _ptr(out))
+    return out

@@ -1,0 +1,252 @@
+"""Pins for the kNN oracle (CPU only). Each test ties oracle/ to something other
+than itself: exact rational arithmetic, lattice closed forms, worked examples
+from the paper/SPEC, invariants of the definition, and scipy's cKDTree (the
+validator the paper itself used)."""
+import numpy as np
+import pytest
+
+from oracle import knn_brute, knn_grid, pair_d2
+from synth import clustered_points, lattice_points, uniform_points
+from tests.exact import brute_exact, canon_d2_exact, to_f32
+
+
+def _rand_f32(n, seed, scale=1.0, offset=0.0):
+    r = np.random.default_rng(seed)
+    return (r.random((n, 3)) * scale + offset).astype(np.float32)
+
+
+# --------------------------------------------------------------------------- exact arithmetic
+
+
+@pytest.mark.parametrize("box", [None, 1.0, (0.75, 1.0, 1.25)])
+def test_brute_equals_exact_rational_definition(box):
+    """Brute force vs. a pure-Python restatement doing every FP32 op in exact
+    rational arithmetic + hand rounding (catches op order, missing FMA, wrap)."""
+    if box is None:
+        pos = _rand_f32(36, 7, scale=0.9, offset=0.05)
+    else:
+        L = np.broadcast_to(np.asarray(box, dtype=np.float32), (3,))
+        pos = (_rand_f32(36, 8) * L).astype(np.float32)
+        pos = np.where(pos >= L, 0, pos).astype(np.float32)
+    k = 7
+    idx, d2 = knn_brute(pos, k, box)
+    ref = brute_exact(pos, k, box)
+    for i in range(len(pos)):
+        assert [j for j, _ in ref[i]] == list(idx[i])
+        assert np.array_equal(np.array([d for _, d in ref[i]], dtype=np.float32).view(np.int32), d2[i].view(np.int32))
+
+
+def test_canonical_formula_uses_fma():
+    """Find pairs where fmaf(dy,dy,dx*dx) differs from RN(RN(dy^2)+RN(dx^2)) and check the
+    oracle returns the fused value (R1)."""
+    r = np.random.default_rng(3)
+    found = 0
+    for _ in range(4000):
+        a = r.random(3).astype(np.float32)
+        b = r.random(3).astype(np.float32)
+        exact = canon_d2_exact(a, b)
+        dx, dy, dz = (np.float32(a[d]) - np.float32(b[d]) for d in range(3))
+        unfused = np.float32(np.float32(np.float32(dx * dx) + np.float32(dy * dy)) + np.float32(dz * dz))
+        if to_f32(exact) != unfused:
+            got = pair_d2(a[None], b[None])[0]
+            assert got.view(np.int32) == to_f32(exact).view(np.int32)
+            found += 1
+            if found >= 5:
+                break
+    assert found >= 5
+
+
+def test_periodic_wrap_convention():
+    """period 10, 0.5 vs 9.5 -> |t| = 1, d2 = 1. Half-open minimal
+    image [-L/2, L/2): t = +L/2 wraps to -L/2, t = -L/2 stays (both give (L/2)^2)."""
+    a = np.array([[0.5, 0, 0]], np.float32)
+    b = np.array([[9.5, 0, 0]], np.float32)
+    assert pair_d2(a, b, 10.0)[0] == 1.0
+    assert pair_d2(b, a, 10.0)[0] == 1.0
+    c = np.array([[5.0, 0, 0]], np.float32)
+    z = np.array([[0.0, 0, 0]], np.float32)
+    assert pair_d2(c, z, 10.0)[0] == 25.0 and pair_d2(z, c, 10.0)[0] == 25.0
+
+
+# --------------------------------------------------------------------------- worked examples
+
+
+def test_spec_worked_examples(golden):
+    g = golden("spec_examples.json")
+    e = g["knn_1d"]
+    pos = np.zeros((3, 3), np.float32)
+    pos[:, 0] = e["x"]
+    idx, d2 = knn_brute(pos, e["k"])
+    for row, want in e["rows"].items():
+        r = int(row)
+        assert [list(x) for x in zip(idx[r].tolist(), d2[r].tolist())] == want
+    e = g["knn_periodic"]
+    pos = np.zeros((2, 3), np.float32)
+    pos[:, 0] = e["x"]
+    idx, d2 = knn_brute(pos, e["k"], box=e["box"])
+    assert idx.tolist() == [[0, 1], [1, 0]]
+    assert d2[:, 1].tolist() == [e["cross_d2"]] * 2
+    # k = 1: every point is its own nearest neighbour
+    p = uniform_points(500, 11, 1.0)
+    idx, d2 = knn_brute(p, 1, 1.0)
+    assert np.array_equal(idx[:, 0], np.arange(500)) and not d2.any()
+
+
+# --------------------------------------------------------------------------- lattice closed forms
+
+# number of integer vectors of squared norm m in Z^3 (OEIS A005875), m = 0..10
+R3 = [1, 6, 12, 8, 6, 24, 24, 0, 12, 30, 24]
+
+
+def _shells_expected(k, h2):
+    out = []
+    for m, c in enumerate(R3):
+        out += [m * h2] * c
+    return np.array(out[:k], dtype=np.float32)
+
+
+@pytest.mark.parametrize("k", [1, 7, 27, 32])
+@pytest.mark.parametrize("fn", [knn_brute, knn_grid])
+def test_periodic_lattice_shells(fn, k):
+    """Periodic dyadic 16^3 lattice (h = 1/16, L = 1): every row's d2 list is the cubic
+    lattice shell sequence r3(m) h^2 (SURVEY.md §8(c) pin 2)."""
+    n, h = 16, 1.0 / 16
+    pos = lattice_points(n, h)
+    idx, d2 = fn(pos, k, 1.0)
+    want = _shells_expected(k, h * h)
+    assert np.array_equal(d2, np.broadcast_to(want, d2.shape))
+    # indices inside the truncated shell are the lowest-index lattice points at those offsets
+    i = 1234
+    ix, iy, iz = i // 256, (i // 16) % 16, i % 16
+    cands = []
+    for dx in range(-3, 4):
+        for dy in range(-3, 4):
+            for dz in range(-3, 4):
+                m = dx * dx + dy * dy + dz * dz
+                j = ((ix + dx) % n) * 256 + ((iy + dy) % n) * 16 + (iz + dz) % n
+                cands.append((m, j))
+    cands.sort()
+    assert idx[i].tolist() == [j for _, j in cands[:k]]
+
+
+def test_open_lattice_corner_shells():
+    """Open 8^3 lattice: the corner (0,0,0) sees 1, 3, 3, 1, 3, 6 points at m = 0..5."""
+    pos = lattice_points(8, 0.125)
+    idx, d2 = knn_grid(pos, 17, None)
+    want = np.array([0] + [1] * 3 + [2] * 3 + [3] * 1 + [4] * 3 + [5] * 6, np.float32) * np.float32(0.125 ** 2)
+    assert np.array_equal(d2[0], want)
+
+
+# --------------------------------------------------------------------------- brute == grid
+
+
+def _sets():
+    yield "uniform", uniform_points(1000, 21, 1.0), 1.0
+    yield "uniform-open", uniform_points(1000, 22, 1.0), None
+    yield "clustered", clustered_points(3000, 23, 1.0), 1.0
+    yield "clustered-open", clustered_points(3000, 24, 1.0), None
+    d = uniform_points(200, 25, 1.0)
+    yield "duplicates", np.concatenate([d, d, d[:50], d[:50]]), 1.0
+    c = np.zeros((300, 3), np.float32)
+    c[:, 0] = uniform_points(300, 26, 1.0)[:, 0]
+    yield "collinear", c, None
+    pl = uniform_points(400, 27, 1.0)
+    pl[:, 2] = 0.25
+    yield "planar", pl, 1.0
+    yield "lattice", lattice_points(8, 0.125), 1.0
+    yield "box-faces", np.array([[0, 0, 0], [0.5, 0.5, 0.5], [0.999, 0, 0], [0, 0.999, 0.999], [0.5, 0, 0.999]] * 4,
+                                np.float32), 1.0
+    yield "anisotropic-box", (uniform_points(800, 28, 1.0) * np.array([2.0, 1.0, 0.5], np.float32)), (2.0, 1.0, 0.5)
+
+
+@pytest.mark.parametrize("name,pos,box", list(_sets()), ids=[s[0] for s in _sets()])
+@pytest.mark.parametrize("k", [1, 8, 16, 32])
+def test_grid_equals_brute(name, pos, box, k):
+    if k > len(pos):
+        pytest.skip("k > n")
+    i1, d1 = knn_brute(pos, k, box)
+    i2, d2 = knn_grid(pos, k, box)
+    assert np.array_equal(i1, i2)
+    assert np.array_equal(d1.view(np.int32), d2.view(np.int32))
+
+
+@pytest.mark.parametrize("n", [1, 2, 8, 9, 33])
+def test_tiny_sizes(n):
+    pos = uniform_points(n, 30 + n, 1.0)
+    for k in sorted({1, min(n, 8), n}):
+        for box in (None, 1.0):
+            i1, d1 = knn_brute(pos, k, box)
+            i2, d2 = knn_grid(pos, k, box)
+            assert np.array_equal(i1, i2) and np.array_equal(d1, d2)
+            assert sorted(set(i1[0].tolist())) == sorted(i1[0].tolist())
+    with pytest.raises(ValueError):
+        knn_brute(pos, n + 1)
+
+
+def test_sampled_rows_match_full():
+    pos = clustered_points(5000, 31, 1.0)
+    rows = np.array([0, 17, 4999, 2500, 17])
+    i_full, d_full = knn_grid(pos, 16, 1.0)
+    i_s, d_s = knn_grid(pos, 16, 1.0, rows=rows)
+    i_b, d_b = knn_brute(pos, 16, 1.0, rows=rows)
+    assert np.array_equal(i_full[rows], i_s) and np.array_equal(i_s, i_b)
+    assert np.array_equal(d_full[rows], d_s) and np.array_equal(d_s, d_b)
+
+
+# --------------------------------------------------------------------------- invariants
+
+
+@pytest.mark.parametrize("box", [None, 1.0])
+def test_invariants(box):
+    pos = clustered_points(4000, 41, 1.0)
+    k = 16
+    idx, d2 = knn_grid(pos, k, box)
+    n = len(pos)
+    # strictly increasing (d2, idx); no repeats
+    for i in range(0, n, 97):
+        row = list(zip(d2[i].tolist(), idx[i].tolist()))
+        assert row == sorted(row) and len(set(idx[i].tolist())) == k
+    # column 0 is self (no exact duplicates in this set)
+    assert np.array_equal(idx[:, 0], np.arange(n)) and not d2[:, 0].any()
+    # stored d2 is the canonical d2 of (p_j, p_i) -- bitwise symmetry
+    a = np.repeat(pos, k, axis=0)
+    b = pos[idx.ravel()]
+    assert np.array_equal(pair_d2(b, a, box).view(np.int32), d2.ravel().view(np.int32))
+    # prefix property: row for k is the prefix of the row for k' > k
+    idx8, d8 = knn_grid(pos, 8, box)
+    assert np.array_equal(idx8, idx[:, :8]) and np.array_equal(d8, d2[:, :8])
+
+
+def test_permutation_equivariance():
+    pos = uniform_points(2000, 51, 1.0)
+    perm = np.random.default_rng(5).permutation(2000)
+    i1, d1 = knn_grid(pos, 8, 1.0)
+    i2, d2 = knn_grid(pos[perm], 8, 1.0)
+    inv = np.argsort(perm)
+    # uniform random f32 data: distance ties are absent, so index sets map exactly
+    assert np.array_equal(d1[perm], d2)
+    assert np.array_equal(perm[i2], i1[perm])
+    assert len(inv) == 2000
+
+
+@pytest.mark.parametrize("box", [None, 1.0])
+def test_scipy_ckdtree_crosscheck(box):
+    """The paper validated against scipy-ckdtree: FP64 distances agree to
+    1e-6 relative, plus (periodic only) an absolute sqrt(3) * ulp(L)/2 for pairs across the
+    boundary -- the canonical formula rounds RN(q - s) before wrapping (R1).
+    Index sets agree except rows with a near-tie at the k-th place."""
+    from scipy.spatial import cKDTree
+
+    pos = clustered_points(20000, 61, 1.0)
+    k = 16
+    idx, d2 = knn_grid(pos, k, box)
+    p64 = pos.astype(np.float64)
+    tree = cKDTree(p64, boxsize=box) if box is not None else cKDTree(p64)
+    dd, ii = tree.query(p64, k=k + 1)
+    abs_tol = 0.0 if box is None else np.sqrt(3.0) * 2.0 ** -25 * box
+    tol = 1e-6 * dd[:, :k] + abs_tol + 1e-30
+    assert np.all(np.abs(np.sqrt(d2.astype(np.float64)) - dd[:, :k]) <= tol)
+    mismatch = [i for i in range(len(pos)) if set(idx[i]) != set(ii[i, :k])]
+    for i in mismatch:  # allowed only for a near-tie at the k-th place
+        assert abs(dd[i, k] - dd[i, k - 1]) <= 2 * tol[i, k - 1]
+    assert len(mismatch) <= 5
