@@ -1,0 +1,195 @@
+/*
+ * jz_knn.h -- C ABI of the B200-native jz-tree exact kNN hot path.
+ *
+ * Problem ("N separate source and query points ... float32",
+ * L453 "query points equal to the source points", L454 "periodic wrapping in
+ * the distance calculation"; BASELINE.json north_star): given N points in 3-D
+ * (FP32), an optional periodic box and k, return for every point the k nearest
+ * points (itself included) as global indices and squared distances, ordered by
+ * (d2, index) ascending. The result is the unique exact answer under the
+ * canonical FP32 distance (R1-R3):
+ *     t_d = RN(q_d - s_d); periodic: t_d >= L_d/2 -> RN(t_d - L_d),
+ *                                    t_d < -L_d/2 -> RN(t_d + L_d);
+ *     d2  = fmaf(t_z, t_z, fmaf(t_y, t_y, t_x * t_x)).
+ *
+ * Method (§2-§3): Morton (z-order) sort with 21-bit-per-axis keys,
+ * plane-based tree hierarchy, dual tree walk NodeToNode per plane
+ * (Alg. 1-3) and LeafToLeaf. All steps run in sm_100a
+ * CUDA kernels; there is no CPU fallback.
+ *
+ * Conventions
+ *  - Pointers are CUDA DEVICE pointers unless marked (host).
+ *  - Calls are ordered on the given stream (jz_stream_t == cudaStream_t; NULL =
+ *    legacy default stream). build/query synchronise the stream internally a few
+ *    times to read data-dependent sizes; outputs are complete when they return.
+ *  - Every int-returning call returns JZ_OK (0) or an error code; on error no
+ *    output is written and jz_last_error() returns a thread-local message.
+ *  - Thread safety: one index must not be used by two threads at once; distinct
+ *    indices are independent.
+ */
+#ifndef JZ_KNN_H
+#define JZ_KNN_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define JZ_API __attribute__((visibility("default")))
+#else
+#define JZ_API
+#endif
+
+typedef struct CUstream_st *jz_stream_t; /* same type as cudaStream_t */
+typedef struct jz_knn_index jz_knn_index;  /* opaque; owns all its device memory */
+
+enum {
+  JZ_OK = 0,
+  JZ_EINVAL = 2,    /* bad argument (n < 1, k < 1, k > n, k > 32, bad box, bad order, NULL pointer) */
+  JZ_EDATA = 3,     /* NaN / Inf coordinate, or periodic coordinate outside [0, L) */
+  JZ_ECAPACITY = 4, /* reserved: internal capacities grow on demand */
+  JZ_ECUDA = 5,     /* CUDA runtime error (message in jz_last_error) */
+  JZ_ENOMEM = 7     /* device allocation failed */
+};
+
+enum { JZ_ORDER_INPUT = 0, JZ_ORDER_Z = 1 };
+
+enum {
+  JZ_FLAG_FRAME = 1u << 0,         /* use frame_origin / frame_extent for the Morton keys (multi-GPU: one global frame) */
+  JZ_FLAG_NO_EARLY_EXIT = 1u << 1, /* disable the sorted-r_low early exit (pruning-safety tests) */
+  JZ_FLAG_NO_SEGSORT = 1u << 2     /* do not sort interaction segments by r_low (implies no early exit) */
+};
+
+/* Tree / walk parameters. Zero fields take the paper's defaults. */
+typedef struct {
+  int32_t nmax0;   /* N_max^(0), leaf capacity; 0 => 48. Range 1..128 */
+  int32_t coarsen; /* c, N_max^(p) = N_max^(0) c^p; 0 => 8. >= 2 */
+  int32_t ntarget; /* N_target: build plane p >= 1 iff 2N / N_max^(p) >= N_target; 0 => 1000 */
+  int32_t ngr;     /* NGR, top nodes per super node; 0 => 32 */
+  uint32_t flags;  /* JZ_FLAG_* */
+  float frame_origin[3]; /* with JZ_FLAG_FRAME: key frame origin (open boundary) */
+  float frame_extent;    /* with JZ_FLAG_FRAME: key frame edge length (> 0) */
+  int32_t reserved[4];
+} jz_knn_params;
+
+/*
+ * Build the tree over n points.
+ *   pos   [n][3] float, xyz row-major (device). The index copies what it needs;
+ *         pos may be freed once the call returns.
+ *   box   (host) [3] periodic box lengths L_d > 0, or NULL for open boundaries.
+ *         Periodic coordinates must satisfy 0 <= x_d < L_d (else JZ_EDATA).
+ *   p     (host) parameters or NULL for defaults.
+ *   out   (host) receives the new index (caller frees with jz_knn_free).
+ * Global index of point i = i. All n points are queries.
+ */
+JZ_API int jz_knn_build(const float *pos, int64_t n, const float *box, const jz_knn_params *p, jz_stream_t s,
+                 jz_knn_index **out);
+
+/*
+ * Build over points that carry their global index: pts4[i] = {x, y, z, bits(gidx)}
+ * (device, float4, gidx an int32 stored bitwise in .w). Only the first n_query
+ * points (in input order) are queries; points [n_query, n) are sources only
+ * (multi-GPU ghosts). jz_knn_rows() returns n_query.
+ */
+JZ_API int jz_knn_build_xyzg(const float *pts4, int64_t n, int64_t n_query, const float *box, const jz_knn_params *p,
+                      jz_stream_t s, jz_knn_index **out);
+
+/* Number of result rows the index produces (host out). */
+JZ_API int jz_knn_rows(const jz_knn_index *ix, int64_t *m);
+
+/*
+ * k nearest neighbours of every query point.
+ *   k        1 <= k <= min(32, n)   (k_max = 32)
+ *   order    JZ_ORDER_INPUT: row i belongs to query point i (input position; for
+ *            jz_knn_build_xyzg: the i-th query point of pts4).
+ *            JZ_ORDER_Z: rows in Morton order; out_row_gidx[r] names the point.
+ *   out_idx  [m][k] int32 global indices (device)
+ *   out_d2   [m][k] float canonical squared distances (device)
+ *   out_row_gidx [m] int32 (device) or NULL; required for JZ_ORDER_Z.
+ * The index is reusable for several queries (construction never depends on k).
+ */
+JZ_API int jz_knn_query(jz_knn_index *ix, int k, int order, int32_t *out_idx, float *out_d2, int32_t *out_row_gidx,
+                 jz_stream_t s);
+
+/* Release the index (synchronises its stream). NULL-safe. */
+JZ_API void jz_knn_free(jz_knn_index *ix);
+
+/*
+ * End-to-end convenience on HOST buffers: copies pos_host to the device, builds,
+ * queries, copies the rows back (input order), frees. pos_host [n][3],
+ * idx_host [n][k], d2_host [n][k]; pinned host memory gives full PCIe speed.
+ */
+JZ_API int jz_knn_search_host(const float *pos_host, int64_t n, const float *box, const jz_knn_params *p, int k,
+                       int32_t *idx_host, float *d2_host, jz_stream_t s);
+
+/*
+ * Per-stage device timings (ms) of the last build + query on this index, for the
+ * phase breakdown of PAPER.md Fig. knnsteps:
+ *   [0] frame+validate [1] sort [2] tree build [3] node-to-node walk [4] leaf-to-leaf [5] total.
+ * Also reports the number of (query, source) distance evaluations of the last query
+ * in *evals (host, may be NULL). Timing is off unless JZ_TIMING=1 in the environment
+ * or jz_set_timing(1) was called.
+ */
+JZ_API int jz_knn_stage_times(const jz_knn_index *ix, float out_ms[6], int64_t *evals);
+JZ_API void jz_set_timing(int on);
+
+/* Number of kernels this library has launched in the process so far. */
+JZ_API int64_t jz_launch_count(void);
+
+/* Thread-local description of the last error. */
+JZ_API const char *jz_last_error(void);
+
+/* ---------------------------------------------------------------------------
+ * Multi-GPU stage entry points. The exchanges between
+ * ranks are done by the caller (torch.distributed over NCCL); these calls do
+ * the per-rank compute on device buffers.
+ * ------------------------------------------------------------------------- */
+
+/* Morton keys of n points in a given frame (origin[3], extent; periodic: pass the
+ * box as origin 0 / extent per axis via box != NULL). keys: [n] uint64 (device). */
+JZ_API int jz_morton_keys(const float *pos, int64_t n, const float *box, const float *origin, float extent,
+                   uint64_t *keys, jz_stream_t s);
+
+/* For each point, the destination rank r such that splitters[r-1] <= key < splitters[r]
+ * (splitters sorted, nsplit = R - 1 entries), plus per-rank counts.
+ *   dest [n] int32 (device), counts [R] int64 (device, overwritten). */
+JZ_API int jz_bucket_by_splitters(const uint64_t *keys, int64_t n, const uint64_t *splitters, int32_t nsplit,
+                           int32_t *dest, int64_t *counts, jz_stream_t s);
+
+/* Stable pack of pos (xyz) + global index base+i into float4 rows grouped by dest rank:
+ * out4 [n][4] (device), offsets [R] (device, exclusive prefix of counts). */
+JZ_API int jz_pack_by_rank(const float *pos, int64_t n, int64_t gidx_base, const int32_t *dest, const int64_t *offsets,
+                    int32_t nranks, float *out4, jz_stream_t s);
+
+/* Number of nodes of a plane (plane < 0: the top plane; 0: leaves). */
+JZ_API int jz_knn_plane_nodes(const jz_knn_index *ix, int plane, int64_t *nnodes);
+
+/* Query boxes for ghost selection: for each node of `plane` (< 0: top plane), its AABB
+ * and the largest R_max^2 of its leaves; R_max^2 bounds the canonical k-th neighbour d2
+ * of every contained query point (FindRmax down to the leaf plane).
+ * boxes [nnodes][8] floats {lo.x, lo.y, lo.z, r2, hi.x, hi.y, hi.z, bits(rank)} (device). */
+JZ_API int jz_knn_query_boxes(jz_knn_index *ix, int k, int plane, int rank, float *boxes, jz_stream_t s);
+
+/* Ghost selection: mask[i] (i in the index's sorted point order) gets bit r set when a
+ * query box of rank r != self_rank can reach point i (exact box bound d_low^2 <= r2,
+ * leaf granularity). counts [nranks] int64 (device) = points flagged per rank.
+ * boxes [nbox][8] as produced by jz_knn_query_boxes (all-gathered). nranks <= 32. */
+JZ_API int jz_knn_select_ghosts(jz_knn_index *ix, const float *boxes, int64_t nbox, int self_rank, int32_t nranks,
+                         int32_t *mask, int64_t *counts, jz_stream_t s);
+
+/* Pack the flagged points (float4 {x, y, z, bits(gidx)}) by destination rank into
+ * out4 at offsets [nranks] (device, exclusive prefix of the counts). */
+JZ_API int jz_knn_pack_ghosts(jz_knn_index *ix, const int32_t *mask, int32_t nranks, const int64_t *offsets, float *out4,
+                       jz_stream_t s);
+
+/* Introspection for stage tests (copies to HOST memory dst, returns bytes needed or -1):
+ * what 0 sorted keys u64[n], 1 sorted float4 points [n], 2 perm i32[n] (sorted -> input),
+ * 3 plane `plane` beg i32[nnodes+1], 4 plane boxes (32 B per node), 5 plane count (int64). */
+JZ_API int64_t jz_knn_debug_copy(const jz_knn_index *ix, int what, int plane, void *dst, int64_t cap);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* JZ_KNN_H */

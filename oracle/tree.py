@@ -24,15 +24,35 @@ BITS = 21  # bits per axis (R4)
 SENTINEL = 64  # level of the two boundary gaps (> any 63-bit key level; R5)
 
 
-def quantize(pos, origin, extent):
-    """q_d = min(floor((x_d - o_d) * 2^21 / E_d), 2^21 - 1), computed in float64 on the
-    exact FP32 inputs (structure only; results never depend on it)."""
-    pos = np.asarray(pos, dtype=np.float64)
-    o = np.broadcast_to(np.asarray(origin, dtype=np.float64), (3,))
-    e = np.broadcast_to(np.asarray(extent, dtype=np.float64), (3,))
-    q = np.floor((pos - o) * (2.0 ** BITS) / e)
-    q = np.clip(q, 0, 2 ** BITS - 1)
-    return q.astype(np.uint64)
+def key_frame(pos, box=None):
+    """Morton frame (R4): periodic -> origin 0, extent L_d per axis; open -> origin =
+    FP32 bbox minimum, extent = the largest FP32 span (cubic cells), 1 if all points coincide.
+    Returns (origin f32[3], scale f32[3]) with scale_d = RN32(2^21 / extent_d)."""
+    pos = np.asarray(pos, dtype=np.float32)
+    if box is not None:
+        L = np.broadcast_to(np.asarray(box, dtype=np.float64), (3,))
+        return np.zeros(3, np.float32), np.array([2.0 ** BITS / l for l in L], dtype=np.float32)
+    lo, hi = pos.min(axis=0), pos.max(axis=0)
+    e = np.float32(max(np.float32(hi[d] - lo[d]) for d in range(3)))
+    if not e > 0:
+        e = np.float32(1.0)
+    return lo.astype(np.float32), np.full(3, np.float32(2.0 ** BITS / float(e)), dtype=np.float32)
+
+
+def quantize(pos, origin, scale_or_extent, is_scale=False):
+    """q_d = min(trunc(max(RN32(RN32(x_d - o_d) * s_d), 0)), 2^21 - 1), all in FP32
+    (R4). Structure only: results never depend on it. With is_scale=False the
+    third argument is the extent E and s = RN32(2^21 / E)."""
+    pos = np.asarray(pos, dtype=np.float32)
+    o = np.broadcast_to(np.asarray(origin, dtype=np.float32), (3,))
+    if is_scale:
+        s = np.broadcast_to(np.asarray(scale_or_extent, dtype=np.float32), (3,))
+    else:
+        e = np.broadcast_to(np.asarray(scale_or_extent, dtype=np.float64), (3,))
+        s = np.array([2.0 ** BITS / v for v in e], dtype=np.float32)
+    v = (pos - o).astype(np.float32) * s
+    v = np.clip(v.astype(np.float32), np.float32(0.0), np.float32(2 ** BITS - 1))
+    return np.trunc(v).astype(np.uint64)
 
 
 def morton_keys(q):

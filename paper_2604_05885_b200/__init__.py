@@ -1,0 +1,151 @@
+"""B200-native exact k-nearest-neighbour search on a Morton plane hierarchy
+(jz-tree, arXiv 2604.05885) -- Python front end of libjzknn.so.
+
+    import torch, paper_2604_05885_b200 as jz
+    pos = torch.rand(10**6, 3, device="cuda")
+    idx, d2 = jz.knn(pos, k=16, box=1.0)          # rows in input order
+
+    ix = jz.KnnIndex(pos, box=1.0)                 # build once (§2)
+    idx, d2 = ix.query(16)                         # query many k (§3)
+    idx, d2, gidx = ix.query(16, order="z")        # z-order rows + their global ids
+
+All compute runs in the library's sm_100a kernels; PyTorch only provides device
+memory and the stream. See include/jz_knn.h for the C ABI.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _binding as B
+from ._binding import JzError, JZ_FLAG_FRAME, JZ_FLAG_NO_EARLY_EXIT, JZ_FLAG_NO_SEGSORT  # noqa: F401
+
+__all__ = ["KnnIndex", "knn", "knn_host", "JzError", "set_timing"]
+
+
+def set_timing(on: bool = True):
+    B.lib().jz_set_timing(1 if on else 0)
+
+
+class KnnIndex:
+    """Tree over `pos` (CUDA float32 [n,3], or [n,4] {x,y,z,bits(gidx)} with n_query)."""
+
+    def __init__(self, pos: torch.Tensor, box=None, params=None, n_query: int | None = None, stream=None):
+        if not (isinstance(pos, torch.Tensor) and pos.is_cuda and pos.dtype == torch.float32):
+            raise TypeError("pos must be a CUDA float32 tensor")
+        pos = pos.contiguous()
+        self._lib = B.lib()
+        self._h = ctypes.c_void_p()
+        self.box = box
+        self.stream = stream
+        prm = B.make_params(params)
+        st = B.stream_ptr(stream)
+        if pos.dim() == 2 and pos.shape[1] == 3:
+            if n_query is not None and n_query != pos.shape[0]:
+                raise ValueError("n_query needs [n,4] xyzg input")
+            B.check(self._lib.jz_knn_build(B.dptr(pos), pos.shape[0], B.box3(box), ctypes.byref(prm), st,
+                                           ctypes.byref(self._h)))
+        elif pos.dim() == 2 and pos.shape[1] == 4:
+            nq = pos.shape[0] if n_query is None else int(n_query)
+            B.check(self._lib.jz_knn_build_xyzg(B.dptr(pos), pos.shape[0], nq, B.box3(box), ctypes.byref(prm), st,
+                                                ctypes.byref(self._h)))
+        else:
+            raise ValueError("pos must be [n,3] or [n,4]")
+        self.n = pos.shape[0]
+        self.device = pos.device
+        m = ctypes.c_int64()
+        B.check(self._lib.jz_knn_rows(self._h, ctypes.byref(m)))
+        self.rows = m.value
+
+    def query(self, k: int, order: str = "input", out=None):
+        """k nearest neighbours of every query point: (idx int32 [m,k], d2 float32 [m,k])
+        (+ row gidx int32 [m] for order="z")."""
+        o = {"input": B.JZ_ORDER_INPUT, "z": B.JZ_ORDER_Z}[order]
+        if out is None:
+            idx = torch.empty((self.rows, k), dtype=torch.int32, device=self.device)
+            d2 = torch.empty((self.rows, k), dtype=torch.float32, device=self.device)
+            rg = torch.empty((self.rows,), dtype=torch.int32, device=self.device) if o == B.JZ_ORDER_Z else None
+        else:
+            idx, d2, rg = out
+        B.check(self._lib.jz_knn_query(self._h, int(k), o, B.dptr(idx), B.dptr(d2),
+                                       B.dptr(rg) if rg is not None else None, B.stream_ptr(self.stream)))
+        return (idx, d2) if o == B.JZ_ORDER_INPUT else (idx, d2, rg)
+
+    def stage_times(self):
+        """Per-phase device ms of the last build + query (needs set_timing(True) before the build)."""
+        t = (ctypes.c_float * 6)()
+        ev = ctypes.c_int64()
+        B.check(self._lib.jz_knn_stage_times(self._h, t, ctypes.byref(ev)))
+        names = ["frame", "sort", "tree", "node2node", "leaf2leaf", "total"]
+        d = {n: float(v) for n, v in zip(names, t)}
+        d["evals"] = ev.value
+        return d
+
+    # ---- introspection (tests)
+    def _copy(self, what, plane=0, dtype=np.uint8):
+        nbytes = self._lib.jz_knn_debug_copy(self._h, what, plane, None, 0)
+        if nbytes < 0:
+            raise ValueError("bad introspection request")
+        buf = np.empty(nbytes, dtype=np.uint8)
+        if nbytes:
+            self._lib.jz_knn_debug_copy(self._h, what, plane, buf.ctypes.data_as(ctypes.c_void_p), nbytes)
+        return buf.view(dtype)
+
+    def sorted_keys(self):
+        return self._copy(0, dtype=np.uint64)
+
+    def sorted_points(self):
+        return self._copy(1, dtype=np.float32).reshape(-1, 4)
+
+    def perm(self):
+        return self._copy(2, dtype=np.int32)
+
+    def num_planes(self):
+        return int(self._copy(5, dtype=np.int64)[0])
+
+    def plane_beg(self, p):
+        return self._copy(3, p, dtype=np.int32)
+
+    def plane_boxes(self, p):
+        return self._copy(4, p, dtype=np.float32).reshape(-1, 8)
+
+    def handle(self):
+        return self._h
+
+    def free(self):
+        if self._h:
+            self._lib.jz_knn_free(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def knn(pos: torch.Tensor, k: int, box=None, order: str = "input", params=None, stream=None):
+    """Exact kNN of every point of `pos` among all points (self included)."""
+    ix = KnnIndex(pos, box=box, params=params, stream=stream)
+    try:
+        return ix.query(k, order=order)
+    finally:
+        ix.free()
+
+
+def knn_host(pos: np.ndarray, k: int, box=None, params=None, out=None, stream=None):
+    """End to end on host arrays through jz_knn_search_host (H2D, build, query, D2H)."""
+    pos = np.ascontiguousarray(pos, dtype=np.float32)
+    n = pos.shape[0]
+    if out is None:
+        idx = np.empty((n, k), dtype=np.int32)
+        d2 = np.empty((n, k), dtype=np.float32)
+    else:
+        idx, d2 = out
+    prm = B.make_params(params)
+    B.check(B.lib().jz_knn_search_host(pos.ctypes.data_as(ctypes.c_void_p), n, B.box3(box), ctypes.byref(prm),
+                                       int(k), idx.ctypes.data_as(ctypes.c_void_p),
+                                       d2.ctypes.data_as(ctypes.c_void_p), B.stream_ptr(stream)))
+    return idx, d2

@@ -1,0 +1,280 @@
+// jz_build.cu -- plane-based tree hierarchy (§2.3).
+//
+//  A4 k_levels       lvl_g = bitlen(key_{g-1} xor key_g) for gaps g in [1, N-1]; lvl_0 = lvl_N = 64
+//                    (integer-key reading DESIGN.md R4/R5).
+//  A5 k_leaf_flags   gap g is a leaf split iff n_g > N_max^(0), decided inside a +-N_max^(0) window
+//                    of gap levels staged in shared memory (P:L253 step (2) "range search"). n_g is
+//                    the distance between the nearest gaps with a strictly greater level on each
+//                    side (equal to the paper's binary-search definition; pinned by
+//                    tests/test_oracle_tree.py::test_node_ranges_equal_nearest_greater).
+//     compaction     scan + scatter -> spl^(0).
+//  A6 k_split_n      exact n at every leaf split by the paper's two binary searches on the
+//                    sorted keys (P:L147-155, P:L253 step (3)).
+//  A7 planes         spl^(p) = leaf splits with n > N_max^(0) c^p, stored as positions in plane
+//                    p-1's split array (Fig. 3); plane p >= 1 exists iff
+//                    2N / N_max^(p) >= N_target.
+//  A8 boxes          exact FP32 AABB + point count per node; leaves reduce over their points,
+//                    coarser planes over their children (R7: AABBs instead of
+//                    Morton-cell centre/level boxes).
+#include <climits>
+#include <vector>
+
+#include "jz_common.cuh"
+#include "jz_internal.h"
+
+namespace jz {
+
+__global__ void k_levels(const uint64_t *__restrict__ keys, int64_t n, uint8_t *__restrict__ lvl) {
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g <= n; g += (int64_t)gridDim.x * blockDim.x) {
+    uint8_t l = kLevelSentinel;
+    if (g > 0 && g < n) l = (uint8_t)(64 - __clzll((long long)(keys[g - 1] ^ keys[g])));
+    lvl[g] = l;
+  }
+}
+
+constexpr int kFlagBlock = 512;
+
+__global__ void __launch_bounds__(kFlagBlock) k_leaf_flags(const uint8_t *__restrict__ lvl, int64_t n, int W,
+                                                           int32_t *__restrict__ flag) {
+  extern __shared__ uint8_t s_l[];
+  const int64_t b0 = (int64_t)blockIdx.x * kFlagBlock;
+  const int64_t w0 = b0 - W;
+  const int len = kFlagBlock + 2 * W + 2;
+  for (int i = threadIdx.x; i < len; i += blockDim.x) {
+    int64_t g = w0 + i;
+    s_l[i] = (g < 0 || g > n) ? (uint8_t)255 : lvl[g];
+  }
+  __syncthreads();
+  const int64_t g = b0 + threadIdx.x;
+  if (g > n) return;
+  int f = 1;
+  if (g > 0 && g < n) {
+    const int li = s_l[g - w0];
+    int64_t L = -1;
+    for (int64_t j = g - 1; j >= g + 1 - W; --j)
+      if (s_l[j - w0] > li) {
+        L = j;
+        break;
+      }
+    if (L >= 0) {
+      int64_t R = -1;
+      for (int64_t j = g + 1; j <= L + W; ++j)
+        if (s_l[j - w0] > li) {
+          R = j;
+          break;
+        }
+      f = R < 0;  // found within the window <=> n = R - L <= N_max^(0)
+    }
+  }
+  flag[g] = f;
+}
+
+__global__ void k_compact_gaps(const int32_t *__restrict__ flag, const int64_t *__restrict__ pos, int64_t m,
+                               int32_t *__restrict__ out) {
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < m; g += (int64_t)gridDim.x * blockDim.x)
+    if (flag[g]) out[pos[g]] = (int32_t)g;
+}
+
+// n at every leaf split by binary search on keys.
+__global__ void k_split_n(const uint64_t *__restrict__ keys, int64_t n, const int32_t *__restrict__ spl,
+                          int64_t nspl, const uint8_t *__restrict__ lvl, int32_t *__restrict__ nsplit) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nspl; j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = spl[j];
+    if (g <= 0 || g >= n) {
+      nsplit[j] = INT_MAX;
+      continue;
+    }
+    const int l = lvl[g];
+    const uint64_t kg = keys[g], kg1 = keys[g - 1];
+    // l_b: smallest a in [0, g-1] with bitlen(key_a ^ key_g) <= l
+    int64_t lo = 0, hi = g - 1;
+    while (lo < hi) {
+      int64_t mid = (lo + hi) >> 1;
+      if (64 - __clzll((long long)(keys[mid] ^ kg)) <= l) hi = mid;
+      else lo = mid + 1;
+    }
+    const int64_t lb = lo;
+    // r_b: smallest r in [g, N) with bitlen(key_{g-1} ^ key_r) > l, N if none
+    lo = g;
+    hi = n;
+    while (lo < hi) {
+      int64_t mid = (lo + hi) >> 1;
+      if (64 - __clzll((long long)(kg1 ^ keys[mid])) > l) hi = mid;
+      else lo = mid + 1;
+    }
+    int64_t v = lo - lb;
+    nsplit[j] = v > INT_MAX ? INT_MAX : (int32_t)v;
+  }
+}
+
+__global__ void k_plane_flags(const int32_t *__restrict__ leafspl_prev, int64_t m, const int32_t *__restrict__ nsplit,
+                              int64_t nmax, int32_t *__restrict__ flag) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += (int64_t)gridDim.x * blockDim.x)
+    flag[j] = (int64_t)nsplit[leafspl_prev[j]] > nmax;
+}
+
+__global__ void k_plane_compact(const int32_t *__restrict__ flag, const int64_t *__restrict__ pos,
+                                const int32_t *__restrict__ leafspl_prev, int64_t m, int32_t *__restrict__ beg,
+                                int32_t *__restrict__ leafspl) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += (int64_t)gridDim.x * blockDim.x)
+    if (flag[j]) {
+      int64_t p = pos[j];
+      beg[p] = (int32_t)j;
+      leafspl[p] = leafspl_prev[j];
+    }
+}
+
+__global__ void k_iota(int32_t *__restrict__ a, int64_t m) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += (int64_t)gridDim.x * blockDim.x)
+    a[j] = (int32_t)j;
+}
+
+// one warp per leaf: AABB of its points + count
+__global__ void k_leaf_boxes(const float4 *__restrict__ pts, const int32_t *__restrict__ beg, int64_t nleaf,
+                             NodeBox *__restrict__ box) {
+  const int lane = threadIdx.x & 31;
+  int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (; w < nleaf; w += nw) {
+    const int b = beg[w], e = beg[w + 1];
+    float lx = INFINITY, ly = INFINITY, lz = INFINITY, hx = -INFINITY, hy = -INFINITY, hz = -INFINITY;
+    for (int i = b + lane; i < e; i += 32) {
+      float4 p = pts[i];
+      lx = fminf(lx, p.x);
+      ly = fminf(ly, p.y);
+      lz = fminf(lz, p.z);
+      hx = fmaxf(hx, p.x);
+      hy = fmaxf(hy, p.y);
+      hz = fmaxf(hz, p.z);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      lx = fminf(lx, __shfl_xor_sync(0xffffffffu, lx, o));
+      ly = fminf(ly, __shfl_xor_sync(0xffffffffu, ly, o));
+      lz = fminf(lz, __shfl_xor_sync(0xffffffffu, lz, o));
+      hx = fmaxf(hx, __shfl_xor_sync(0xffffffffu, hx, o));
+      hy = fmaxf(hy, __shfl_xor_sync(0xffffffffu, hy, o));
+      hz = fmaxf(hz, __shfl_xor_sync(0xffffffffu, hz, o));
+    }
+    if (lane == 0) {
+      NodeBox nb;
+      nb.lo = make_float4(lx, ly, lz, __int_as_float(e - b));
+      nb.hi = make_float4(hx, hy, hz, 0.f);
+      box[w] = nb;
+    }
+  }
+}
+
+// one warp per node of plane p: AABB over its children in plane p-1
+__global__ void k_node_boxes(const NodeBox *__restrict__ child, const int32_t *__restrict__ beg, int64_t nnodes,
+                             NodeBox *__restrict__ box) {
+  const int lane = threadIdx.x & 31;
+  int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (; w < nnodes; w += nw) {
+    const int b = beg[w], e = beg[w + 1];
+    float lx = INFINITY, ly = INFINITY, lz = INFINITY, hx = -INFINITY, hy = -INFINITY, hz = -INFINITY;
+    int cnt = 0;
+    for (int i = b + lane; i < e; i += 32) {
+      NodeBox c = child[i];
+      lx = fminf(lx, c.lo.x);
+      ly = fminf(ly, c.lo.y);
+      lz = fminf(lz, c.lo.z);
+      hx = fmaxf(hx, c.hi.x);
+      hy = fmaxf(hy, c.hi.y);
+      hz = fmaxf(hz, c.hi.z);
+      cnt += __float_as_int(c.lo.w);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      lx = fminf(lx, __shfl_xor_sync(0xffffffffu, lx, o));
+      ly = fminf(ly, __shfl_xor_sync(0xffffffffu, ly, o));
+      lz = fminf(lz, __shfl_xor_sync(0xffffffffu, lz, o));
+      hx = fmaxf(hx, __shfl_xor_sync(0xffffffffu, hx, o));
+      hy = fmaxf(hy, __shfl_xor_sync(0xffffffffu, hy, o));
+      hz = fmaxf(hz, __shfl_xor_sync(0xffffffffu, hz, o));
+      cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    }
+    if (lane == 0) {
+      NodeBox nb;
+      nb.lo = make_float4(lx, ly, lz, __int_as_float(cnt));
+      nb.hi = make_float4(hx, hy, hz, 0.f);
+      box[w] = nb;
+    }
+  }
+}
+
+void free_planes(std::vector<Plane> &planes, cudaStream_t st) {
+  for (auto &p : planes) {
+    if (p.beg) cudaFreeAsync(p.beg, st);
+    if (p.leafspl) cudaFreeAsync(p.leafspl, st);
+    if (p.box) cudaFreeAsync(p.box, st);
+    p = Plane();
+  }
+  planes.clear();
+}
+
+void build_planes(const uint64_t *keys, const float4 *pts, int64_t n, const jz_knn_params_t &prm,
+                  std::vector<Plane> &planes, cudaStream_t st) {
+  const int W = prm.nmax0;
+  uint8_t *lvl = nullptr;
+  int32_t *flag = nullptr;
+  int64_t *pos = nullptr;
+  JZ_CUDA(cudaMallocAsync(&lvl, (n + 1) * sizeof(uint8_t), st));
+  JZ_CUDA(cudaMallocAsync(&flag, (n + 1) * sizeof(int32_t), st));
+  JZ_CUDA(cudaMallocAsync(&pos, (n + 2) * sizeof(int64_t), st));
+  k_levels<<<grid_for(n + 1, 256), 256, 0, st>>>(keys, n, lvl);
+  JZ_LAUNCH_CHECK();
+  const unsigned fb = (unsigned)ceil_div(n + 1, kFlagBlock);
+  k_leaf_flags<<<fb, kFlagBlock, kFlagBlock + 2 * W + 2, st>>>(lvl, n, W, flag);
+  JZ_LAUNCH_CHECK();
+  exclusive_scan_i32_to_i64(flag, pos, n + 1, st);
+  const int64_t nspl = read_i64(pos + (n + 1), st);  // = N_leaf + 1
+  Plane leaf;
+  leaf.nnodes = nspl - 1;
+  leaf.nmax = W;
+  JZ_CUDA(cudaMallocAsync(&leaf.beg, nspl * sizeof(int32_t), st));
+  JZ_CUDA(cudaMallocAsync(&leaf.leafspl, nspl * sizeof(int32_t), st));
+  JZ_CUDA(cudaMallocAsync(&leaf.box, leaf.nnodes * sizeof(NodeBox), st));
+  k_compact_gaps<<<grid_for(n + 1, 256), 256, 0, st>>>(flag, pos, n + 1, leaf.beg);
+  JZ_LAUNCH_CHECK();
+  k_iota<<<grid_for(nspl, 256), 256, 0, st>>>(leaf.leafspl, nspl);
+  JZ_LAUNCH_CHECK();
+  int32_t *nsplit = nullptr;
+  JZ_CUDA(cudaMallocAsync(&nsplit, nspl * sizeof(int32_t), st));
+  k_split_n<<<grid_for(nspl, 128), 128, 0, st>>>(keys, n, leaf.beg, nspl, lvl, nsplit);
+  JZ_LAUNCH_CHECK();
+  k_leaf_boxes<<<grid_for(leaf.nnodes * 32, 256), 256, 0, st>>>(pts, leaf.beg, leaf.nnodes, leaf.box);
+  JZ_LAUNCH_CHECK();
+  planes.push_back(leaf);
+  // coarser planes
+  int64_t nmax = W;
+  while (true) {
+    if (nmax > (int64_t)INT_MAX / prm.coarsen) break;
+    nmax *= prm.coarsen;
+    if (2.0 * (double)n / (double)nmax < (double)prm.ntarget) break;
+    const Plane &pv = planes.back();
+    const int64_t m = pv.nnodes + 1;
+    k_plane_flags<<<grid_for(m, 256), 256, 0, st>>>(pv.leafspl, m, nsplit, nmax, flag);
+    JZ_LAUNCH_CHECK();
+    exclusive_scan_i32_to_i64(flag, pos, m, st);
+    const int64_t np1 = read_i64(pos + m, st);
+    Plane pl;
+    pl.nnodes = np1 - 1;
+    pl.nmax = nmax;
+    JZ_CUDA(cudaMallocAsync(&pl.beg, np1 * sizeof(int32_t), st));
+    JZ_CUDA(cudaMallocAsync(&pl.leafspl, np1 * sizeof(int32_t), st));
+    JZ_CUDA(cudaMallocAsync(&pl.box, pl.nnodes * sizeof(NodeBox), st));
+    k_plane_compact<<<grid_for(m, 256), 256, 0, st>>>(flag, pos, pv.leafspl, m, pl.beg, pl.leafspl);
+    JZ_LAUNCH_CHECK();
+    k_node_boxes<<<grid_for(pl.nnodes * 32, 256), 256, 0, st>>>(pv.box, pl.beg, pl.nnodes, pl.box);
+    JZ_LAUNCH_CHECK();
+    planes.push_back(pl);
+  }
+  JZ_CUDA(cudaFreeAsync(nsplit, st));
+  JZ_CUDA(cudaFreeAsync(lvl, st));
+  JZ_CUDA(cudaFreeAsync(flag, st));
+  JZ_CUDA(cudaFreeAsync(pos, st));
+}
+
+}  // namespace jz

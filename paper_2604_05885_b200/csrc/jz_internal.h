@@ -1,0 +1,88 @@
+// jz_internal.h -- host-side structures of the CUDA path (index, planes, interaction lists).
+#pragma once
+#include <cstdint>
+#include <vector>
+
+#include "../../include/jz_knn.h"
+#include "jz_common.cuh"
+
+typedef jz_knn_params jz_knn_params_t;
+
+namespace jz {
+
+// One tree plane (a set of nodes partitioning the points).
+//   p = 0 (leaves): beg[i] = first point of leaf i (spl^(0)), beg[nnodes] = N.
+//   p >= 1       : beg[i] = first child (a node of plane p-1) of node i (spl^(p) as positions
+//                  in plane p-1's split array, P:L224 / Fig. 3 spl^(1) = {0,2,4,5}).
+struct Plane {
+  int64_t nnodes = 0;
+  int64_t nmax = 0;
+  int32_t *beg = nullptr;     // [nnodes + 1] (device)
+  int32_t *leafspl = nullptr; // [nnodes + 1] index into the leaf split array (device); p = 0: identity
+  NodeBox *box = nullptr;     // [nnodes] (device)
+};
+
+struct Stage {
+  cudaEvent_t ev[8] = {};
+  bool on = false;
+};
+
+// build (jz_sort.cu)
+void compute_frame(const float *pos, int64_t n, int stride, const Dom &D, const jz_knn_params_t &prm, Frame *frame,
+                   cudaStream_t st);
+void sort_points(const float *pos, int64_t n, int stride, int gidx_mode, int64_t gidx_base, const Frame &frame,
+                 uint64_t *keys_out, int32_t *perm_out, float4 *pts_out, cudaStream_t st);
+void morton_keys(const float *pos, int64_t n, const Frame &f, uint64_t *keys, cudaStream_t st);
+
+// tree (jz_build.cu)
+void build_planes(const uint64_t *keys, const float4 *pts, int64_t n, const jz_knn_params_t &prm,
+                  std::vector<Plane> &planes, cudaStream_t st);
+void free_planes(std::vector<Plane> &planes, cudaStream_t st);
+
+// walk (jz_walk.cu)
+struct IList {
+  int64_t nrecv = 0, total = 0;
+  int64_t *ispl = nullptr;  // [nrecv + 1]
+  int32_t *isrc = nullptr;  // [total]
+  float *rlow = nullptr;    // [total]  squared lower bound d_low^2 of the (receiver, source) pair
+  void release(cudaStream_t st);
+};
+// Walk the plane hierarchy down to the leaf plane (Alg. 1 lines 1-5).
+// Returns the leaf interaction list and R_max^2 per leaf (rmax2_leaf, device, caller frees).
+void walk_to_leaves(const std::vector<Plane> &planes, const Dom &D, int k, int ngr, unsigned flags, IList &leaf_il,
+                    float **rmax2_leaf, cudaStream_t st);
+
+// leaf-to-leaf (jz_leaf.cu)
+struct LeafArgs {
+  const float4 *pts;
+  const int32_t *leaf_beg;
+  const NodeBox *leaf_box;
+  const IList *il;
+  const float *rmax2;
+  const int32_t *perm;    // sorted position -> input position
+  const int32_t *zrow;    // sorted position -> z-order query row (nullptr: identity)
+  int64_t nleaf;
+  int64_t n_query;        // input positions < n_query are queries
+  int k;
+  int order;
+  int nmax0;
+  unsigned flags;
+  int32_t *out_idx;
+  float *out_d2;
+  int32_t *out_row_gidx;
+  unsigned long long *evals;  // device counter (may be nullptr)
+};
+void leaf_to_leaf(const LeafArgs &a, const Dom &D, cudaStream_t st);
+
+// read-only view of an index for the multi-GPU stage kernels (jz_dist.cu)
+struct IndexView {
+  int64_t n;
+  const float4 *pts;
+  const std::vector<Plane> *planes;
+  Dom D;
+  int ngr;
+  unsigned flags;
+};
+IndexView view_of(const jz_knn_index *ix);
+
+}  // namespace jz

@@ -1,0 +1,311 @@
+// jz_walk.cu -- dual tree walk down the plane hierarchy (
+// PAPER.md Alg. 1 lines 1-5 L309-322, Alg. 2 NodeToNode L337-352, Alg. 3 FindRmax L354-384,
+// early exit on sorted r_low L395-398).
+//
+// Layout: an interaction list at plane level p is (ispl [nrecv+1] int64, isrc int32, rlow f32)
+// with rlow = d_low^2 of the (receiver, source) pair. Receivers at level p+1 are "parents";
+// the kernels below move the list one plane down:
+//   k_n2n<RMAX>   one CTA per receiving parent, one thread per child: a register
+//                 count-heap of N_r = 8 (d_up^2, count) entries over the children of
+//                 every source parent in the segment, staged in shared memory -> R_max^2.
+//   k_n2n<COUNT>  #source children with d_low^2 <= R_max^2
+//   scan          CumulativeSumPrep0 (jz_scan.cu)
+//   k_n2n<INSERT> write isrc / rlow at the scanned offsets
+//   k_segsort     sort each receiver's segment by (rlow, isrc) (P:L396 bitonic network).
+// All bounds are squared FP32 values that bound the canonical d2 exactly (jz_common.cuh).
+#include <climits>
+#include <vector>
+
+#include "jz_common.cuh"
+#include "jz_internal.h"
+
+namespace jz {
+
+constexpr int kN2NThreads = 64;
+constexpr int kN2NStage = 256;  // source children staged per round (8 KB)
+constexpr int kHeap = 8;        // N_r (R13)
+
+enum { RMAX = 0, COUNT = 1, INSERT = 2 };
+
+void IList::release(cudaStream_t st) {
+  if (ispl) cudaFreeAsync(ispl, st);
+  if (isrc) cudaFreeAsync(isrc, st);
+  if (rlow) cudaFreeAsync(rlow, st);
+  ispl = nullptr;
+  isrc = nullptr;
+  rlow = nullptr;
+  nrecv = total = 0;
+}
+
+__global__ void k_dense_init(int64_t S, int64_t *__restrict__ ispl, int32_t *__restrict__ isrc,
+                             float *__restrict__ rlow) {
+  // ispl_i = S i, isrc_j = j mod S; r_low = 0 at the top
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < S * S; j += (int64_t)gridDim.x * blockDim.x) {
+    isrc[j] = (int32_t)(j % S);
+    rlow[j] = 0.f;
+    if (j <= S) ispl[j] = S * j;
+  }
+}
+
+__global__ void k_super_beg(int64_t S, int64_t ntop, int ngr, int32_t *__restrict__ beg) {
+  // Alg. 1 line 1: spl^(P) = Range(0, N_top, NGR)
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j <= S; j += (int64_t)gridDim.x * blockDim.x)
+    beg[j] = (int32_t)min(j * ngr, ntop);
+}
+
+// ---- count heap: 8 slots sorted by radius, empty slots = (+inf, 0)
+struct CountHeap {
+  float r[kHeap];
+  int c[kHeap];
+  int tot;
+};
+
+__device__ __forceinline__ float heap_radius(const CountHeap &h, int k) {
+  int cum = 0;
+  float R = INFINITY;
+  bool found = false;
+#pragma unroll
+  for (int j = 0; j < kHeap; ++j) {
+    cum += h.c[j];
+    if (!found && cum >= k) {
+      R = h.r[j];
+      found = true;
+    }
+  }
+  return R;
+}
+
+__device__ __forceinline__ void heap_insert(CountHeap &h, float r, int c, int k) {
+  if (h.c[kHeap - 1] == 0 || h.tot - h.c[kHeap - 1] + c >= k) {
+    // ordered insert after equal radii, discarding the last slot
+    h.tot += c - h.c[kHeap - 1];
+#pragma unroll
+    for (int j = kHeap - 1; j > 0; --j) {
+      const bool mv = h.r[j - 1] > r;
+      const bool here = !mv && h.r[j] > r;
+      h.r[j] = mv ? h.r[j - 1] : (here ? r : h.r[j]);
+      h.c[j] = mv ? h.c[j - 1] : (here ? c : h.c[j]);
+    }
+    if (h.r[0] > r) {
+      h.r[0] = r;
+      h.c[0] = c;
+    }
+  } else {
+    // dropping the last would leave < k: add the count to the first larger radius
+    bool done = false;
+#pragma unroll
+    for (int j = 0; j < kHeap; ++j) {
+      if (!done && h.r[j] > r) {
+        h.c[j] += c;
+        done = true;
+      }
+    }
+    if (!done) {  // no larger radius: the last slot absorbs it at radius r (R13)
+      h.r[kHeap - 1] = r;
+      h.c[kHeap - 1] += c;
+    }
+    h.tot += c;
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kN2NThreads) k_n2n(const int32_t *__restrict__ pbeg, const int64_t *__restrict__ ispl,
+                                                     const int32_t *__restrict__ isrc, const float *__restrict__ rlow,
+                                                     const NodeBox *__restrict__ cbox, Dom D, int k, int sorted,
+                                                     int early, float *__restrict__ rmax2, int32_t *__restrict__ cnt,
+                                                     const int64_t *__restrict__ ispl_out,
+                                                     int32_t *__restrict__ isrc_out, float *__restrict__ rlow_out) {
+  __shared__ NodeBox s_box[kN2NStage];
+  __shared__ float s_red[kN2NThreads / 32];
+  const int J = blockIdx.x;
+  const int cb = pbeg[J], ce = pbeg[J + 1];
+  const int64_t eb = ispl[J], ee = ispl[J + 1];
+  for (int c0 = cb; c0 < ce; c0 += kN2NThreads) {
+    const int i = c0 + threadIdx.x;
+    const bool valid = i < ce;
+    NodeBox mb;
+    if (valid) mb = cbox[i];
+    CountHeap h;
+    float R = INFINITY;
+    int count = 0;
+    int64_t wp = 0;
+    float Rchunk = 0.f;
+    if (MODE == RMAX) {
+#pragma unroll
+      for (int j = 0; j < kHeap; ++j) {
+        h.r[j] = INFINITY;
+        h.c[j] = 0;
+      }
+      h.tot = 0;
+    } else {
+      R = valid ? rmax2[i] : 0.f;
+      if (MODE == INSERT && valid) wp = ispl_out[i];
+      float m = R;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+      if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = m;
+      __syncthreads();
+      Rchunk = s_red[0];
+#pragma unroll
+      for (int w = 1; w < kN2NThreads / 32; ++w) Rchunk = fmaxf(Rchunk, s_red[w]);
+    }
+    for (int64_t e = eb; e < ee; ++e) {
+      const int S = isrc[e];
+      const float rl = rlow[e];
+      if (early) {
+        // early exit: no child can use this entry (d_low of children >= rl)
+        bool need;
+        if (MODE == RMAX) need = __syncthreads_or(valid && rl < R);
+        else need = rl <= Rchunk;
+        if (!need) {
+          if (sorted) break;
+          continue;
+        }
+      }
+      const int sb = pbeg[S], se = pbeg[S + 1];
+      for (int s0 = sb; s0 < se; s0 += kN2NStage) {
+        const int sn = min(kN2NStage, se - s0);
+        __syncthreads();
+        for (int t = threadIdx.x; t < sn; t += kN2NThreads) s_box[t] = cbox[s0 + t];
+        __syncthreads();
+        if (valid) {
+          for (int t = 0; t < sn; ++t) {
+            const NodeBox sbx = s_box[t];
+            if (MODE == RMAX) {
+              const float r2 = box_dup2(mb, sbx, D);
+              if (r2 < R) {
+                heap_insert(h, r2, box_count(sbx), k);
+                R = heap_radius(h, k);
+              }
+            } else {
+              const float dl = box_dlow2(mb, sbx, D);
+              if (dl <= R) {
+                if (MODE == COUNT) ++count;
+                else {
+                  isrc_out[wp] = s0 + t;
+                  rlow_out[wp] = dl;
+                  ++wp;
+                }
+              }
+            }
+          }
+        }
+      }
+    }
+    if (valid) {
+      if (MODE == RMAX) rmax2[i] = R;
+      if (MODE == COUNT) cnt[i] = count;
+    }
+    __syncthreads();
+  }
+}
+
+// ---- segment sort: one warp per receiver, bitonic network in shared memory
+constexpr int kSegMax = 1024;
+constexpr int kSegWarps = 4;
+
+__global__ void __launch_bounds__(kSegWarps * 32) k_segsort(const int64_t *__restrict__ ispl, int64_t nrecv,
+                                                          int32_t *__restrict__ isrc, float *__restrict__ rlow) {
+  __shared__ unsigned long long s_k[kSegWarps][kSegMax];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  unsigned long long *sk = s_k[w];
+  for (int64_t seg = (int64_t)blockIdx.x * kSegWarps + w; seg < nrecv; seg += (int64_t)gridDim.x * kSegWarps) {
+    const int64_t b = ispl[seg];
+    const int m = (int)(ispl[seg + 1] - b);
+    if (m <= 1) continue;
+    if (m > kSegMax) {
+      // too long to sort here: r_low = 0 is a valid lower bound and trivially sorted
+      for (int i = lane; i < m; i += 32) rlow[b + i] = 0.f;
+      continue;
+    }
+    int P = 32;
+    while (P < m) P <<= 1;
+    for (int i = lane; i < P; i += 32)
+      sk[i] = i < m ? (((unsigned long long)__float_as_uint(rlow[b + i]) << 32) | (unsigned)isrc[b + i]) : ~0ull;
+    __syncwarp();
+    for (int size = 2; size <= P; size <<= 1) {
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int i = lane; i < (P >> 1); i += 32) {
+          const int lo = 2 * stride * (i / stride) + (i % stride);
+          const int hi = lo + stride;
+          const bool asc = (lo & size) == 0;
+          unsigned long long x = sk[lo], y = sk[hi];
+          if ((x > y) == asc) {
+            sk[lo] = y;
+            sk[hi] = x;
+          }
+        }
+        __syncwarp();
+      }
+    }
+    for (int i = lane; i < m; i += 32) {
+      unsigned long long v = sk[i];
+      isrc[b + i] = (int32_t)(v & 0xffffffffu);
+      rlow[b + i] = __uint_as_float((unsigned)(v >> 32));
+    }
+    __syncwarp();
+  }
+}
+
+void walk_to_leaves(const std::vector<Plane> &planes, const Dom &D, int k, int ngr, unsigned flags, IList &leaf_il,
+                    float **rmax2_leaf, cudaStream_t st) {
+  const int P = (int)planes.size();
+  const int top = P - 1;
+  const int64_t ntop = planes[top].nnodes;
+  const int64_t S = ceil_div(ntop, ngr);
+  const bool early = !(flags & JZ_FLAG_NO_EARLY_EXIT);
+  const bool do_sort = !(flags & JZ_FLAG_NO_SEGSORT);
+  int32_t *superbeg = nullptr;
+  JZ_CUDA(cudaMallocAsync(&superbeg, (S + 1) * sizeof(int32_t), st));
+  k_super_beg<<<grid_for(S + 1, 256), 256, 0, st>>>(S, ntop, ngr, superbeg);
+  JZ_LAUNCH_CHECK();
+  IList il;
+  il.nrecv = S;
+  il.total = S * S;
+  JZ_CUDA(cudaMallocAsync(&il.ispl, (S + 1) * sizeof(int64_t), st));
+  JZ_CUDA(cudaMallocAsync(&il.isrc, il.total * sizeof(int32_t), st));
+  JZ_CUDA(cudaMallocAsync(&il.rlow, il.total * sizeof(float), st));
+  k_dense_init<<<grid_for(S * S + 1, 256), 256, 0, st>>>(S, il.ispl, il.isrc, il.rlow);
+  JZ_LAUNCH_CHECK();
+  for (int p = top; p >= 0; --p) {
+    const int32_t *pbeg = (p == top) ? superbeg : planes[p + 1].beg;
+    const int64_t npar = (p == top) ? S : planes[p + 1].nnodes;
+    const Plane &pl = planes[p];
+    float *rmax2 = nullptr;
+    int32_t *cnt = nullptr;
+    JZ_CUDA(cudaMallocAsync(&rmax2, pl.nnodes * sizeof(float), st));
+    JZ_CUDA(cudaMallocAsync(&cnt, pl.nnodes * sizeof(int32_t), st));
+    const int srt = do_sort ? 1 : 0;
+    const int ee = early ? 1 : 0;
+    k_n2n<RMAX><<<(unsigned)npar, kN2NThreads, 0, st>>>(pbeg, il.ispl, il.isrc, il.rlow, pl.box, D, k, srt, ee,
+                                                        rmax2, nullptr, nullptr, nullptr, nullptr);
+    JZ_LAUNCH_CHECK();
+    k_n2n<COUNT><<<(unsigned)npar, kN2NThreads, 0, st>>>(pbeg, il.ispl, il.isrc, il.rlow, pl.box, D, k, srt, ee,
+                                                         rmax2, cnt, nullptr, nullptr, nullptr);
+    JZ_LAUNCH_CHECK();
+    IList nl;
+    nl.nrecv = pl.nnodes;
+    JZ_CUDA(cudaMallocAsync(&nl.ispl, (pl.nnodes + 1) * sizeof(int64_t), st));
+    exclusive_scan_i32_to_i64(cnt, nl.ispl, pl.nnodes, st);
+    nl.total = read_i64(nl.ispl + pl.nnodes, st);
+    JZ_CUDA(cudaMallocAsync(&nl.isrc, (nl.total > 0 ? nl.total : 1) * sizeof(int32_t), st));
+    JZ_CUDA(cudaMallocAsync(&nl.rlow, (nl.total > 0 ? nl.total : 1) * sizeof(float), st));
+    k_n2n<INSERT><<<(unsigned)npar, kN2NThreads, 0, st>>>(pbeg, il.ispl, il.isrc, il.rlow, pl.box, D, k, srt, ee,
+                                                          rmax2, nullptr, nl.ispl, nl.isrc, nl.rlow);
+    JZ_LAUNCH_CHECK();
+    if (do_sort) {
+      k_segsort<<<grid_for(pl.nnodes, kSegWarps, 148 * 16), kSegWarps * 32, 0, st>>>(nl.ispl, nl.nrecv, nl.isrc,
+                                                                                     nl.rlow);
+      JZ_LAUNCH_CHECK();
+    }
+    il.release(st);
+    il = nl;
+    JZ_CUDA(cudaFreeAsync(cnt, st));
+    if (p > 0) JZ_CUDA(cudaFreeAsync(rmax2, st));
+    else *rmax2_leaf = rmax2;
+  }
+  JZ_CUDA(cudaFreeAsync(superbeg, st));
+  leaf_il = il;
+}
+
+}  // namespace jz

@@ -1,0 +1,282 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the oracle, element by element.
+
+Bar (BASELINE.json north_star): indices bit-exact (ties -> lower index), squared
+distances within 1e-6 relative -- asserted here as bit-exact, which the canonical
+FP32 formula makes well posed (R1-R3). Sizes span several sort tiles
+(3072 keys) and ragged tails; the full-size C4 config is checked on sampled rows.
+"""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from oracle import knn_brute, knn_grid  # noqa: E402
+from oracle import tree as T  # noqa: E402
+from synth import clustered_points, lattice_points, make_config, uniform_points  # noqa: E402
+
+
+def _jz():
+    import paper_2604_05885_b200 as jz
+
+    return jz
+
+
+def _gpu_knn(pos, k, box, order="input", params=None):
+    jz = _jz()
+    t = torch.from_numpy(np.ascontiguousarray(pos, dtype=np.float32)).cuda()
+    ix = jz.KnnIndex(t, box=box, params=params)
+    out = ix.query(k, order=order)
+    res = tuple(o.cpu().numpy() for o in out)
+    ix.free()
+    return res
+
+
+def _assert_same(idx_g, d2_g, idx_o, d2_o):
+    assert idx_g.shape == idx_o.shape
+    bad = np.nonzero((idx_g != idx_o).any(axis=1) | (d2_g.view(np.int32) != d2_o.view(np.int32)).any(axis=1))[0]
+    assert bad.size == 0, f"{bad.size} rows differ, first {bad[:5]}: gpu {idx_g[bad[0]]} {d2_g[bad[0]]} " \
+                          f"oracle {idx_o[bad[0]]} {d2_o[bad[0]]}"
+
+
+def _assert_rel(d2_g, d2_o, tol=1e-6):
+    assert np.all(np.abs(d2_g.astype(np.float64) - d2_o) <= tol * np.abs(d2_o.astype(np.float64)))
+
+
+# ----------------------------------------------------------------------------------- C1
+
+
+def test_c1_config_bit_exact():
+    """C1: 4096 uniform points, unit periodic box, k = 8 vs the brute-force oracle."""
+    pos, box, k = make_config("C1")
+    ig, dg = _gpu_knn(pos, k, box)
+    io, do = knn_brute(pos, k, box)
+    _assert_same(ig, dg, io, do)
+    _assert_rel(dg, do)
+
+
+def _sets():
+    yield "uniform", uniform_points(5000, 21, 1.0), 1.0
+    yield "uniform-open", uniform_points(5000, 22, 1.0), None
+    yield "clustered", clustered_points(8000, 23, 1.0), 1.0
+    yield "clustered-open", clustered_points(8000, 24, 1.0), None
+    d = uniform_points(700, 25, 1.0)
+    yield "duplicates", np.concatenate([d, d, d[:100], d[:100], np.repeat(d[:2], 200, axis=0)]), 1.0
+    c = np.zeros((1500, 3), np.float32)
+    c[:, 0] = uniform_points(1500, 26, 1.0)[:, 0]
+    yield "collinear", c, None
+    pl = uniform_points(2000, 27, 1.0)
+    pl[:, 2] = 0.25
+    yield "planar", pl, 1.0
+    yield "lattice-periodic", lattice_points(16, 1.0 / 16), 1.0
+    yield "lattice-open", lattice_points(12, 0.125), None
+    yield "box-faces", np.array([[0, 0, 0], [0.5, 0.5, 0.5], [0.999, 0, 0], [0, 0.999, 0.999], [0.5, 0, 0.999]] * 20,
+                                np.float32), 1.0
+    yield "anisotropic-box", (uniform_points(3000, 28, 1.0) * np.array([2.0, 1.0, 0.5], np.float32)), (2.0, 1.0, 0.5)
+    yield "negative-open", (uniform_points(3000, 29, 1.0) * 8 - 5).astype(np.float32), None
+    yield "all-identical", np.full((300, 3), 0.375, np.float32), 1.0
+
+
+@pytest.mark.parametrize("name,pos,box", list(_sets()), ids=[s[0] for s in _sets()])
+@pytest.mark.parametrize("k", [1, 8, 16, 32])
+def test_parity_sets(name, pos, box, k):
+    if k > len(pos):
+        pytest.skip("k > n")
+    ig, dg = _gpu_knn(pos, k, box)
+    io, do = knn_grid(pos, k, box)
+    _assert_same(ig, dg, io, do)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 17, 33, 100, 3071, 3072, 3073, 9217, 65537])
+@pytest.mark.parametrize("box", [None, 1.0])
+def test_parity_sizes(n, box):
+    """Ragged sizes around the radix-sort tile (3072) and warp widths."""
+    pos = clustered_points(n, 100 + n, 1.0) if n > 1000 else uniform_points(n, 100 + n, 1.0)
+    for k in sorted({1, min(n, 5), min(n, 16), min(n, 32)}):
+        ig, dg = _gpu_knn(pos, k, box)
+        io, do = knn_grid(pos, k, box)
+        _assert_same(ig, dg, io, do)
+
+
+@pytest.mark.parametrize("params", [dict(nmax0=1), dict(nmax0=8, coarsen=2, ntarget=4), dict(nmax0=32),
+                                    dict(nmax0=64, coarsen=3, ntarget=10), dict(nmax0=128), dict(ngr=1),
+                                    dict(nmax0=16, coarsen=2, ntarget=1, ngr=3)])
+def test_parity_params(params):
+    """Tree shape parameters change the walk, never the result."""
+    pos = clustered_points(20000, 7, 1.0)
+    for box in (1.0, None):
+        ig, dg = _gpu_knn(pos, 16, box, params=params)
+        io, do = knn_grid(pos, 16, box)
+        _assert_same(ig, dg, io, do)
+
+
+def test_pruning_safety():
+    """Disabling the r_low early exit and the segment sort changes no output bit."""
+    jz = _jz()
+    pos = clustered_points(30000, 8, 1.0)
+    ref = _gpu_knn(pos, 16, 1.0)
+    for flags in (jz.JZ_FLAG_NO_EARLY_EXIT, jz.JZ_FLAG_NO_SEGSORT, jz.JZ_FLAG_NO_EARLY_EXIT | jz.JZ_FLAG_NO_SEGSORT):
+        got = _gpu_knn(pos, 16, 1.0, params=dict(flags=flags))
+        assert np.array_equal(ref[0], got[0]) and np.array_equal(ref[1].view(np.int32), got[1].view(np.int32))
+
+
+def test_z_order_rows():
+    pos = uniform_points(20000, 9, 1.0)
+    ii, di = _gpu_knn(pos, 8, 1.0)
+    iz, dz, gz = _gpu_knn(pos, 8, 1.0, order="z")
+    assert sorted(gz.tolist()) == list(range(20000))
+    assert np.array_equal(iz, ii[gz]) and np.array_equal(dz, di[gz])
+    # z order: Morton keys of the rows are non-decreasing
+    o, s = T.key_frame(pos, 1.0)
+    keys = T.morton_keys(T.quantize(pos[gz], o, s, is_scale=True))
+    assert np.all(np.diff(keys.astype(np.float64)) >= 0) or np.all(keys[1:] >= keys[:-1])
+
+
+def test_query_reuse_and_determinism():
+    jz = _jz()
+    pos = clustered_points(50000, 10, 1.0)
+    t = torch.from_numpy(pos).cuda()
+    ix = jz.KnnIndex(t, box=1.0)
+    a = [tuple(x.cpu().numpy() for x in ix.query(k)) for k in (16, 8, 16, 32)]
+    assert np.array_equal(a[0][0], a[2][0]) and np.array_equal(a[0][1], a[2][1])
+    # prefix property across k
+    assert np.array_equal(a[1][0], a[0][0][:, :8]) and np.array_equal(a[0][0], a[3][0][:, :16])
+    ix.free()
+
+
+def test_host_entry_point():
+    jz = _jz()
+    pos = clustered_points(30000, 11, 1.0)
+    ih, dh = jz.knn_host(pos, 16, box=1.0)
+    ig, dg = _gpu_knn(pos, 16, 1.0)
+    assert np.array_equal(ih, ig) and np.array_equal(dh, dg)
+
+
+def test_errors():
+    jz = _jz()
+    good = torch.from_numpy(uniform_points(100, 12, 1.0)).cuda()
+    with pytest.raises(jz.JzError) as e:
+        jz.knn(good, 33, box=1.0)
+    assert e.value.code == 2
+    with pytest.raises(jz.JzError) as e:
+        jz.knn(good[:5], 6, box=1.0)
+    assert e.value.code == 2
+    bad = good.clone()
+    bad[7, 1] = float("nan")
+    with pytest.raises(jz.JzError) as e:
+        jz.knn(bad, 4)
+    assert e.value.code == 3
+    out = good.clone()
+    out[3, 0] = 1.0  # periodic coordinate must be < L
+    with pytest.raises(jz.JzError) as e:
+        jz.knn(out, 4, box=1.0)
+    assert e.value.code == 3
+    with pytest.raises(jz.JzError) as e:
+        jz.knn(good, 4, box=(1.0, -1.0, 1.0))
+    assert e.value.code == 2
+    assert jz.knn(out, 4)[0].shape == (100, 4)  # fine without a box
+
+
+# ----------------------------------------------------------------------------------- stages
+
+
+def test_stage_keys_and_sort():
+    """A2/A3: GPU keys equal the oracle's Morton keys (same FP32 quantisation, R4)
+    and the order is the stable sort of (key, input index)."""
+    jz = _jz()
+    for box in (1.0, None):
+        pos = clustered_points(40000, 13, 1.0)
+        if box is None:
+            pos = (pos * 3 - 1).astype(np.float32)
+        ix = jz.KnnIndex(torch.from_numpy(pos).cuda(), box=box)
+        o, s = T.key_frame(pos, box)
+        want = T.morton_keys(T.quantize(pos, o, s, is_scale=True))
+        order = np.argsort(want, kind="stable")
+        assert np.array_equal(ix.perm(), order)
+        assert np.array_equal(ix.sorted_keys(), want[order])
+        sp = ix.sorted_points()
+        assert np.array_equal(sp[:, :3], pos[order])
+        assert np.array_equal(sp[:, 3].view(np.int32), order.astype(np.int32))
+        ix.free()
+
+
+@pytest.mark.parametrize("kind", ["uniform", "clustered", "dups"])
+def test_stage_planes_vs_oracle_tree(kind):
+    """A4-A7: leaf splits and every coarser plane equal the oracle's hierarchy built by the
+    paper's definitions (binary searches, n > N_max^(p)) on the same sorted keys."""
+    jz = _jz()
+    if kind == "uniform":
+        pos = uniform_points(2500, 14, 1.0)
+    elif kind == "clustered":
+        pos = clustered_points(2500, 15, 1.0)
+    else:
+        p = uniform_points(500, 16, 1.0)
+        pos = np.concatenate([p, p, p[:60], np.repeat(p[:1], 90, axis=0)])
+    prm = dict(nmax0=8, coarsen=3, ntarget=20)
+    ix = jz.KnnIndex(torch.from_numpy(pos).cuda(), box=1.0, params=prm)
+    keys = ix.sorted_keys()
+    spl0, planes, _ = T.build_hierarchy(keys, nmax0=8, c=3, ntarget=20)
+    assert ix.num_planes() == 1 + len(planes)
+    assert ix.plane_beg(0).tolist() == spl0
+    for p, want in enumerate(planes, start=1):
+        assert ix.plane_beg(p).tolist() == want
+    # A8: boxes are the exact AABBs of the node's points, counts match
+    sp = ix.sorted_points()
+    beg = ix.plane_beg(0)
+    bx = ix.plane_boxes(0)
+    for i in range(len(beg) - 1):
+        pts = sp[beg[i]:beg[i + 1], :3]
+        assert np.array_equal(bx[i, :3], pts.min(axis=0)) and np.array_equal(bx[i, 4:7], pts.max(axis=0))
+        assert bx[i, 3:4].view(np.int32)[0] == beg[i + 1] - beg[i]
+    ix.free()
+
+
+# ----------------------------------------------------------------------------------- larger configs
+
+
+def test_c2_config_full():
+    """C2: 10^6 uniform, open boundary, k = 16: every row vs the grid oracle."""
+    pos, box, k = make_config("C2")
+    ig, dg = _gpu_knn(pos, k, box)
+    io, do = knn_grid(pos, k, box)
+    _assert_same(ig, dg, io, do)
+
+
+def test_c3_config_sampled():
+    """C3: 10^7 clustered, periodic, k = 32: 20000 sampled rows vs the oracle, invariants on all."""
+    pos, box, k = make_config("C3")
+    ig, dg = _gpu_knn(pos, k, box)
+    rows = np.random.default_rng(3).choice(len(pos), 20000, replace=False)
+    io, do = knn_grid(pos, k, box, rows=rows)
+    _assert_same(ig[rows], dg[rows], io, do)
+    _check_invariants(ig, dg)
+
+
+def _check_invariants(idx, d2):
+    n = idx.shape[0]
+    assert np.all(idx >= 0) and np.all(idx < n)
+    assert np.all(d2[:, 1:] >= d2[:, :-1])
+    tie = d2[:, 1:] == d2[:, :-1]
+    assert np.all(idx[:, 1:][tie] > idx[:, :-1][tie])
+    assert np.all(d2[:, 0] == 0)
+
+
+def test_c4_full_size_sampled():
+    """C4 at its full size (10^8 clustered, periodic, k = 16) in the bench's launch
+    configuration: sampled rows vs the grid oracle, plus invariants on every row (on device)."""
+    jz = _jz()
+    pos, box, k = make_config("C4")
+    t = torch.from_numpy(pos).cuda()
+    ix = jz.KnnIndex(t, box=box)
+    idx, d2 = ix.query(k)
+    ix.free()
+    rows = np.random.default_rng(4).choice(len(pos), 3000, replace=False)
+    io, do = knn_grid(pos, k, box, rows=rows)
+    _assert_same(idx[torch.from_numpy(rows).cuda()].cpu().numpy(), d2[torch.from_numpy(rows).cuda()].cpu().numpy(),
+                 io, do)
+    # invariants on all 10^8 rows, evaluated on the device
+    assert bool((idx >= 0).all()) and bool((idx < len(pos)).all())
+    assert bool((d2[:, 1:] >= d2[:, :-1]).all())
+    tie = d2[:, 1:] == d2[:, :-1]
+    assert bool((idx[:, 1:][tie] > idx[:, :-1][tie]).all())
+    assert bool((d2[:, 0] == 0).all())
