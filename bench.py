@@ -1,0 +1,273 @@
+#!/usr/bin/env python
+"""Benchmark: exact kNN points/s (BASELINE.json metric) on the C4 workload.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C4]
+
+A step is one pass of the whole hot path: build the tree over
+the synthetic input (frame, Morton sort, planes) and answer the k-NN query for every
+point (node-to-node walk + leaf-to-leaf, rows written in input order), inputs resident
+in HBM. N = 1: C4 = 10^8 clustered points, periodic unit box, k = 16 (fits one B200).
+N > 1 (torchrun): the same 10^8-point set, Morton-range partitioned across ranks with a
+ghost exchange (paper_2604_05885_b200/dist.py), strong scaling, max over ranks.
+
+--impl reference times the CPU oracle (oracle/, grid search) on the host cores on a
+bounded sample of the same workload (rank 0 only); see DESIGN.md "Measurement".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "exact kNN points/sec (k=16, 10^8 pts)"
+UNIT = "points/s"
+FP32_OPS_PER_EVAL = 6  # 3 FADD + 1 FMUL + 2 FFMA
+SM_COUNT = 148
+FP32_LANES_PER_SM = 128
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "fallback": True}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    def __init__(self, gpu_index=0):
+        self.gpu = gpu_index
+        self.samples = []
+        self._stop = threading.Event()
+        self._th = None
+
+    def start(self):
+        def run():
+            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+            try:
+                p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                      "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            except OSError:
+                return
+            while not self._stop.is_set():
+                line = p.stdout.readline()
+                if not line:
+                    break
+                self.samples.append([x.strip() for x in line.split(",")])
+            p.terminate()
+
+        self._th = threading.Thread(target=run, daemon=True)
+        self._th.start()
+        time.sleep(0.3)
+
+    def stop(self):
+        self._stop.set()
+        if self._th:
+            self._th.join(timeout=2)
+        if not self.samples:
+            return None
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 2 + i and s[2 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def _config(name, n_override=None):
+    from synth import CONFIGS, make_config
+
+    c = CONFIGS[name]
+    t0 = time.time()
+    pos, box, k = make_config(name, n=n_override)
+    return pos, box, k, c, time.time() - t0
+
+
+def cpu_baseline(pos, box, k, sample_rows=200_000, seed=0):
+    """The oracle (grid search, as it stands) on the host cores: grid build over the full set
+    plus a random sample of query rows; projected to the full row count."""
+    from oracle import knn_grid, oracle_threads
+
+    n = pos.shape[0]
+    rows = np.random.default_rng(seed).choice(n, min(sample_rows, n), replace=False)
+    t0 = time.perf_counter()
+    knn_grid(pos, k, box, rows=rows[:0])
+    t_build = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    knn_grid(pos, k, box, rows=rows)
+    t_all = time.perf_counter() - t0
+    t_q = max(t_all - t_build, 1e-9)
+    t_full = t_build + t_q * n / len(rows)
+    return {"value": n / t_full, "unit": UNIT, "cores": oracle_threads(), "kind": "oracle",
+            "sample": f"oracle grid search on the C4 set: grid over all {n} points ({t_build:.2f} s) + "
+                      f"{len(rows)} random query rows ({t_q:.2f} s), projected to all {n} rows "
+                      f"({t_full:.1f} s)"}, t_full
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle timed on the host cores, rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    pos, box, k, c, _ = _config(args.config, args.n)
+    for _ in range(args.warmup):
+        cpu_baseline(pos, box, k, sample_rows=args.ref_rows, seed=1)
+    vals, times = [], []
+    cb = None
+    for s in range(args.steps):
+        cb, t_full = cpu_baseline(pos, box, k, sample_rows=args.ref_rows, seed=2 + s)
+        vals.append(cb["value"])
+        times.append(t_full)
+    v = float(np.median(vals))
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * float(np.median(times)), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": args.config, "n_points": int(pos.shape[0]), "k": k,
+                       "box": "periodic L=1" if box else "open", "distribution": c["kind"]},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cb["cores"], "kind": "oracle", "sample": cb["sample"]},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_single(args):
+    import torch
+
+    import paper_2604_05885_b200 as jz
+    from paper_2604_05885_b200 import _binding as B
+
+    pos, box, k, c, t_gen = _config(args.config, args.n)
+    n = pos.shape[0]
+    dev = torch.device("cuda:0")
+    st = torch.cuda.current_stream()
+    d_pos = torch.from_numpy(pos).to(dev)
+    idx = torch.empty((n, k), dtype=torch.int32, device=dev)
+    d2 = torch.empty((n, k), dtype=torch.float32, device=dev)
+    jz.set_timing(True)
+
+    def step():
+        ix = jz.KnnIndex(d_pos, box=box)
+        ix.query(k, out=(idx, d2, None))
+        t = ix.stage_times()
+        ix.free()
+        return t
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    lib = B.lib()
+    l0 = lib.jz_launch_count()
+    clk = ClockSampler(0)
+    if not args.profile:
+        clk.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(st)
+    stages = []
+    for _ in range(args.steps):
+        stages.append(step())
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    clocks = clk.stop() if not args.profile else None
+    launches = (lib.jz_launch_count() - l0) // args.steps
+    value = n / (ms / 1e3)
+    keys = ["frame", "sort", "tree", "node2node", "leaf2leaf"]
+    st_ms = {kk: float(np.mean([s[kk] for s in stages])) for kk in keys}
+    evals = int(np.mean([s["evals"] for s in stages]))
+    dominant = max(keys, key=lambda kk: st_ms[kk])
+    peaks = _peaks()
+    clk_mhz = peaks.get("sm_max_mhz", 1965.0)
+    fp32_peak = SM_COUNT * FP32_LANES_PER_SM * clk_mhz * 1e6 / 1e12  # T lane-ops/s
+    l2l_s = st_ms["leaf2leaf"] / 1e3
+    achieved = evals * FP32_OPS_PER_EVAL / l2l_s / 1e12 if l2l_s > 0 else 0.0
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "leaf2leaf_dram_bytes.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "alu", "kernel": "k_leaf2leaf (LeafToLeaf)", "achieved": achieved, "peak": fp32_peak,
+                "unit": "T FP32 lane-ops/s", "frac": achieved / fp32_peak, "traffic": traffic,
+                "peak_source": f"derived: {SM_COUNT} SMs x {FP32_LANES_PER_SM} FP32 lanes x {clk_mhz:.0f} MHz "
+                               "(MEASURED_PEAKS sm_max_mhz); FFMA microbenchmark on this pool measured 36.1-37.0 "
+                               "(profiles/r01_fp32_pipe_microbench.log)",
+                "work": f"{evals} distance evaluations x {FP32_OPS_PER_EVAL} FP32 ops per launch",
+                "ms_per_launch": st_ms["leaf2leaf"], "share_of_step": st_ms["leaf2leaf"] / ms}
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": args.config, "n_points": n, "k": k, "box": "periodic L=1" if box else "open",
+                       "distribution": c["kind"], "order": "input",
+                       "l2": "inputs (1.2 GB positions, 12.8 GB outputs) exceed the 126 MB L2; no flush"},
+            "roofline": roofline, "stages_ms": st_ms, "dominant_stage": dominant, "evals_per_query": evals / n,
+            "gpu_launches": int(launches * args.steps), "clocks": clocks}
+    if not args.profile and not args.no_e2e:
+        line["e2e"] = run_e2e(args, pos, box, k)
+    if not args.profile and not args.no_cpu_baseline:
+        line["cpu_baseline"], _ = cpu_baseline(pos, box, k, sample_rows=args.ref_rows)
+    print(json.dumps(line), flush=True)
+
+
+def run_e2e(args, pos, box, k):
+    """Same metric through jz_knn_search_host: pinned host input, H2D + build + query + D2H."""
+    import torch
+
+    import paper_2604_05885_b200 as jz
+
+    n = pos.shape[0]
+    h_pos = torch.from_numpy(pos).pin_memory()
+    h_idx = torch.empty((n, k), dtype=torch.int32).pin_memory()
+    h_d2 = torch.empty((n, k), dtype=torch.float32).pin_memory()
+    a, b, c = h_pos.numpy(), h_idx.numpy(), h_d2.numpy()
+    jz.knn_host(a, k, box=box, out=(b, c))
+    steps = max(1, min(args.steps, 3))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        jz.knn_host(a, k, box=box, out=(b, c))
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / steps
+    return {"value": n / dt, "unit": UNIT, "h2d_bytes_per_step": int(n * 12), "d2h_bytes_per_step": int(n * k * 8),
+            "ms_per_step": dt * 1e3, "api": "jz_knn_search_host (pinned host buffers)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--n", type=int, default=None, help="override the point count (tests)")
+    ap.add_argument("--ref-rows", type=int, default=200_000)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="kernel-only run for ncu (no e2e / baseline / clocks)")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1:
+        from paper_2604_05885_b200.dist import run_bench_distributed
+
+        run_bench_distributed(args, METRIC, UNIT)
+    else:
+        run_single(args)
+
+
+if __name__ == "__main__":
+    main()

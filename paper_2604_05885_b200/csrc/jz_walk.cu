@@ -40,9 +40,12 @@ void IList::release(cudaStream_t st) {
 __global__ void k_dense_init(int64_t S, int64_t *__restrict__ ispl, int32_t *__restrict__ isrc,
                              float *__restrict__ rlow) {
   // ispl_i = S i, isrc_j = j mod S; r_low = 0 at the top
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < S * S; j += (int64_t)gridDim.x * blockDim.x) {
-    isrc[j] = (int32_t)(j % S);
-    rlow[j] = 0.f;
+  const int64_t m = S * S > S + 1 ? S * S : S + 1;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += (int64_t)gridDim.x * blockDim.x) {
+    if (j < S * S) {
+      isrc[j] = (int32_t)(j % S);
+      rlow[j] = 0.f;
+    }
     if (j <= S) ispl[j] = S * j;
   }
 }
@@ -265,7 +268,7 @@ void walk_to_leaves(const std::vector<Plane> &planes, const Dom &D, int k, int n
   JZ_CUDA(cudaMallocAsync(&il.ispl, (S + 1) * sizeof(int64_t), st));
   JZ_CUDA(cudaMallocAsync(&il.isrc, il.total * sizeof(int32_t), st));
   JZ_CUDA(cudaMallocAsync(&il.rlow, il.total * sizeof(float), st));
-  k_dense_init<<<grid_for(S * S + 1, 256), 256, 0, st>>>(S, il.ispl, il.isrc, il.rlow);
+  k_dense_init<<<grid_for(S * S + 2, 256), 256, 0, st>>>(S, il.ispl, il.isrc, il.rlow);
   JZ_LAUNCH_CHECK();
   for (int p = top; p >= 0; --p) {
     const int32_t *pbeg = (p == top) ? superbeg : planes[p + 1].beg;
