@@ -186,6 +186,7 @@ def run_single(args):
     keys = ["frame", "sort", "tree", "node2node", "leaf2leaf"]
     st_ms = {kk: float(np.mean([s[kk] for s in stages])) for kk in keys}
     evals = int(np.mean([s["evals"] for s in stages]))
+    inserts = int(np.mean([s.get("inserts", 0) for s in stages]))
     dominant = max(keys, key=lambda kk: st_ms[kk])
     peaks = _peaks()
     clk_mhz = peaks.get("sm_max_mhz", 1965.0)
@@ -212,7 +213,7 @@ def run_single(args):
             "config": {"workload": args.config, "n_points": n, "k": k, "box": "periodic L=1" if box else "open",
                        "distribution": c["kind"], "order": "input",
                        "l2": "inputs (1.2 GB positions, 12.8 GB outputs) exceed the 126 MB L2; no flush"},
-            "roofline": roofline, "stages_ms": st_ms, "dominant_stage": dominant, "evals_per_query": evals / n,
+            "roofline": roofline, "stages_ms": st_ms, "dominant_stage": dominant, "evals_per_query": evals / n, "inserts_per_query": inserts / n,
             "gpu_launches": int(launches * args.steps), "clocks": clocks}
     if not args.profile and not args.no_e2e:
         line["e2e"] = run_e2e(args, pos, box, k)

@@ -81,6 +81,9 @@ class KnnIndex:
         names = ["frame", "sort", "tree", "node2node", "leaf2leaf", "total"]
         d = {n: float(v) for n, v in zip(names, t)}
         d["evals"] = ev.value
+        st = (ctypes.c_int64 * 4)()
+        B.check(self._lib.jz_knn_stats(self._h, st))
+        d["inserts"], d["leaves"], d["planes"] = st[1], st[2], st[3]
         return d
 
     # ---- introspection (tests)

@@ -26,7 +26,7 @@ struct jz_knn_index {
   cudaEvent_t ev[8] = {};
   bool timing = false;
   float times[6] = {0, 0, 0, 0, 0, 0};
-  long long evals = 0;
+  long long evals = 0, inserts = 0;
   unsigned long long *d_evals = nullptr;
 };
 
@@ -231,23 +231,27 @@ int jz_knn_query(jz_knn_index *ix, int k, int order, int32_t *out_idx, float *ou
   rec(ix, 4);
   jz::IList il;
   float *rmax2 = nullptr;
-  jz::walk_to_leaves(ix->planes, ix->D, k, ix->prm.ngr, ix->prm.flags, il, &rmax2, st);
+  int32_t *superbeg = nullptr;
+  // walk down to plane 1: its nodes are the receiving parents of LeafToLeaf (jz_leaf.cu)
+  jz::walk_to(ix->planes, ix->D, k, ix->prm.ngr, ix->prm.flags, 1, il, &rmax2, &superbeg, st);
   rec(ix, 5);
-  if (!ix->d_evals) JZ_CUDA(cudaMallocAsync(&ix->d_evals, sizeof(unsigned long long), st));
-  JZ_CUDA(cudaMemsetAsync(ix->d_evals, 0, sizeof(unsigned long long), st));
+  if (!ix->d_evals) JZ_CUDA(cudaMallocAsync(&ix->d_evals, 2 * sizeof(unsigned long long), st));
+  JZ_CUDA(cudaMemsetAsync(ix->d_evals, 0, 2 * sizeof(unsigned long long), st));
+  const bool one_plane = ix->planes.size() == 1;
   jz::LeafArgs la;
   la.pts = ix->pts;
   la.leaf_beg = ix->planes[0].beg;
   la.leaf_box = ix->planes[0].box;
+  la.par_leaf = one_plane ? superbeg : ix->planes[1].beg;
+  la.par_box = one_plane ? nullptr : ix->planes[1].box;
+  la.npar = il.nrecv;
   la.il = &il;
   la.rmax2 = rmax2;
   la.perm = ix->perm;
   la.zrow = ix->zrow;
-  la.nleaf = ix->planes[0].nnodes;
   la.n_query = ix->n_query;
   la.k = k;
   la.order = order;
-  la.nmax0 = ix->prm.nmax0;
   la.flags = ix->prm.flags;
   la.out_idx = out_idx;
   la.out_d2 = out_d2;
@@ -256,11 +260,13 @@ int jz_knn_query(jz_knn_index *ix, int k, int order, int32_t *out_idx, float *ou
   jz::leaf_to_leaf(la, ix->D, st);
   rec(ix, 6);
   il.release(st);
-  JZ_CUDA(cudaFreeAsync(rmax2, st));
-  unsigned long long ev = 0;
-  JZ_CUDA(cudaMemcpyAsync(&ev, ix->d_evals, sizeof(ev), cudaMemcpyDeviceToHost, st));
+  if (rmax2) JZ_CUDA(cudaFreeAsync(rmax2, st));
+  if (superbeg) JZ_CUDA(cudaFreeAsync(superbeg, st));
+  unsigned long long ev[2] = {0, 0};
+  JZ_CUDA(cudaMemcpyAsync(ev, ix->d_evals, sizeof(ev), cudaMemcpyDeviceToHost, st));
   JZ_CUDA(cudaStreamSynchronize(st));
-  ix->evals = (long long)ev;
+  ix->evals = (long long)ev[0];
+  ix->inserts = (long long)ev[1];
   if (ix->timing) {
     cudaEventElapsedTime(&ix->times[3], ix->ev[4], ix->ev[5]);
     cudaEventElapsedTime(&ix->times[4], ix->ev[5], ix->ev[6]);
@@ -318,6 +324,15 @@ int jz_knn_search_host(const float *pos_host, int64_t n, const float *box, const
   JZ_CUDA(cudaStreamSynchronize(st));
   return rc;
   JZ_API_END
+}
+
+int jz_knn_stats(const jz_knn_index *ix, int64_t out[4]) {
+  if (!ix || !out) return fail(JZ_EINVAL, "NULL argument");
+  out[0] = ix->evals;
+  out[1] = ix->inserts;
+  out[2] = ix->planes.empty() ? 0 : ix->planes[0].nnodes;
+  out[3] = (int64_t)ix->planes.size();
+  return JZ_OK;
 }
 
 int jz_knn_stage_times(const jz_knn_index *ix, float out_ms[6], int64_t *evals) {

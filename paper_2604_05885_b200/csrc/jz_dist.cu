@@ -256,7 +256,8 @@ int jz_knn_query_boxes(jz_knn_index *ix, int k, int plane, int rank, float *boxe
       JZ_CUDA(cudaMemcpyAsync(rmax2, inf.data(), inf.size() * sizeof(float), cudaMemcpyHostToDevice, st));
       JZ_CUDA(cudaStreamSynchronize(st));
     } else {
-      jz::walk_to_leaves(pl, v.D, k, v.ngr, v.flags, il, &rmax2, st);
+      int32_t *sb = nullptr;
+      jz::walk_to(pl, v.D, k, v.ngr, v.flags, 0, il, &rmax2, &sb, st);
       il.release(st);
     }
     jz::k_plane_qboxes<<<jz::grid_for(pl[plane].nnodes, 128), 128, 0, st>>>(pl[plane].box, pl[plane].leafspl,

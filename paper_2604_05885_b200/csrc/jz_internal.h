@@ -47,25 +47,30 @@ struct IList {
   float *rlow = nullptr;    // [total]  squared lower bound d_low^2 of the (receiver, source) pair
   void release(cudaStream_t st);
 };
-// Walk the plane hierarchy down to the leaf plane (Alg. 1 lines 1-5).
-// Returns the leaf interaction list and R_max^2 per leaf (rmax2_leaf, device, caller frees).
-void walk_to_leaves(const std::vector<Plane> &planes, const Dom &D, int k, int ngr, unsigned flags, IList &leaf_il,
-                    float **rmax2_leaf, cudaStream_t st);
+// Walk the plane hierarchy from the super nodes down to plane `stop` (Alg. 1
+// lines 1-5): returns the interaction list whose receivers are the nodes of plane `stop`
+// and R_max^2 of those nodes (caller frees). If stop > top plane (only possible for a
+// one-plane tree and stop = 1), the receivers are the super nodes: *superbeg (first top
+// node of each super node, caller frees) is set, the list is the dense one and
+// *rmax2 = nullptr (= +inf).
+void walk_to(const std::vector<Plane> &planes, const Dom &D, int k, int ngr, unsigned flags, int stop, IList &il,
+             float **rmax2, int32_t **superbeg, cudaStream_t st);
 
 // leaf-to-leaf (jz_leaf.cu)
 struct LeafArgs {
   const float4 *pts;
-  const int32_t *leaf_beg;
-  const NodeBox *leaf_box;
-  const IList *il;
-  const float *rmax2;
-  const int32_t *perm;    // sorted position -> input position
-  const int32_t *zrow;    // sorted position -> z-order query row (nullptr: identity)
-  int64_t nleaf;
-  int64_t n_query;        // input positions < n_query are queries
+  const int32_t *leaf_beg;  // [nleaf+1]
+  const NodeBox *leaf_box;  // [nleaf]
+  const int32_t *par_leaf;  // [npar+1] first leaf of each receiving parent
+  const NodeBox *par_box;   // [npar] or nullptr
+  int64_t npar;
+  const IList *il;          // receivers = parents
+  const float *rmax2;       // [npar] or nullptr
+  const int32_t *perm;      // sorted position -> input position
+  const int32_t *zrow;      // sorted position -> z-order query row (nullptr: identity)
+  int64_t n_query;          // input positions < n_query are queries
   int k;
   int order;
-  int nmax0;
   unsigned flags;
   int32_t *out_idx;
   float *out_d2;

@@ -1,28 +1,67 @@
 // jz_leaf.cu -- LeafToLeaf (Alg. 1 line 6 L321, L386, L398).
 //
-// One warp per (query leaf, chunk of 32 queries); one query point per lane. The warp
-// walks its leaf's interaction list in r_low order; before each entry it takes the warp max of
-// the lanes' current k-th squared distance and stops once r_low exceeds it (P:L398 early exit,
-// "maximum current estimate ... across all threads"). The source leaf's float4 points
-// {x, y, z, bits(gidx)} are staged in the warp's shared-memory slot with coalesced 16-byte
-// loads and read back as broadcasts. Each lane keeps a sorted register top-k of 64-bit keys
-// (d2_bits << 32 | gidx + 1): unsigned order == (d2, index) lexicographic order since d2 >= 0,
-// so ties go to the lower global index (R2). The list starts full of sentinels at
-// the leaf's R_max^2, which bounds every contained query's true k-th distance, so candidates
-// beyond it are never inserted. Periodic boxes: per (query leaf, source leaf) pair each axis is
-// classified from the two AABBs as "all pairs wrap by -L / +L / none" (then the shift is one
-// exact FADD) or "straddles" (per-pair select); both reproduce the definition bit for bit.
-// The epilogue writes each row straight to its final place (input order or z-order), so there
-// is no separate reorder pass.
+// B200 design:
+//  * Work item = 32 consecutive (z-order) query points of one receiving plane-1 node J, one
+//    query per lane, one warp per item; warps are independent (no CTA barriers).
+//    The item walks J's plane-1 interaction list (sorted by r_low): the leaf-level
+//    NodeToNode pass is not materialised. Leaf pairs are pruned on the fly: the bounding box
+//    of the warp's queries is tested against each source node S and then, one lane per child
+//    leaf, against S's child leaves (a ballot gives the survivors), with the exact monotone
+//    d_low^2 bound against the warp's current max k-th distance (the early exit of P:L398).
+//  * Surviving leaves are staged by the warp into its own shared-memory slot as separate
+//    x / y / z / gidx arrays (coalesced 16-byte loads, leaf starts aligned to 4, tails padded
+//    with NaN coordinates so their d2 is NaN and never passes a comparison).
+//  * Distances: two sources per packed f32x2 instruction, query coordinate as the broadcast
+//    operand: FADD2 x3, FMUL2, FFMA2 x2 per source pair = the canonical scalar formula with
+//    per-element round-to-nearest (bit-identical). Periodic leaf pairs whose pairs all wrap
+//    the same way get one extra exact FADD2 per axis; straddling pairs use the per-pair select.
+//  * Filtering: per group of 4 sources the lane compares min(d2) with its k-th distance; the
+//    insertion slow path runs only when some lane passes. Top-k: sorted register list of
+//    64-bit keys (d2_bits << 32 | gidx + 1): unsigned order == (d2, index) order (R2),
+//    initialised with sentinels at R_max^2 of J (bounds every contained query's k-th distance).
+//  * Rows are written straight to their final place (input or z order): no reorder pass.
 #include "jz_common.cuh"
 #include "jz_internal.h"
 
 namespace jz {
 
-constexpr int kLeafWarps = 4;
+constexpr int kLWarps = 4;
+constexpr int kLThreads = kLWarps * 32;
+constexpr int kLCap = 256;  // staged source points per warp (4 KB SoA)
+
+typedef unsigned long long u64;
+
+__device__ __forceinline__ u64 pk(float lo, float hi) {
+  u64 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void upk(u64 v, float &lo, float &hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ u64 sub2(u64 a, u64 b) {
+  u64 d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ u64 add2(u64 a, u64 b) {
+  u64 d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ u64 mul2(u64 a, u64 b) {
+  u64 d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c) {
+  u64 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
 
 template <int K>
-__device__ __forceinline__ void topk_insert(unsigned long long (&a)[K], unsigned long long key) {
+__device__ __forceinline__ void topk_insert(u64 (&a)[K], u64 key) {
 #pragma unroll
   for (int j = K - 1; j > 0; --j) {
     const bool mv = key < a[j - 1];
@@ -32,152 +71,249 @@ __device__ __forceinline__ void topk_insert(unsigned long long (&a)[K], unsigned
   if (key < a[0]) a[0] = key;
 }
 
-struct LeafK {
+struct LeafPK {
   const float4 *pts;
-  const int32_t *leaf_beg;
-  const NodeBox *leaf_box;
-  const int64_t *ispl;
+  const int32_t *leaf_beg;   // [nleaf+1] first point of each leaf
+  const NodeBox *leaf_box;   // [nleaf]
+  const int32_t *par_leaf;   // [npar+1] first leaf of each receiving parent
+  const NodeBox *par_box;    // [npar] or nullptr
+  const int64_t *ispl;       // parent-level interaction list
   const int32_t *isrc;
   const float *rlow;
-  const float *rmax2;
+  const float *rmax2;        // [npar] or nullptr (= +inf)
+  const int32_t *item_par;   // [nitems] receiving parent of each 32-query work item
+  const int32_t *item_q0;    // [nitems] first query (sorted position) of the item
+  int64_t nitems;
   const int32_t *perm;
   const int32_t *zrow;
-  int64_t nleaf;
   int64_t n_query;
   int k;
   int order;
-  int nmax0;
-  int chunks;
   int early;
   int sorted;
   int32_t *out_idx;
   float *out_d2;
   int32_t *out_row_gidx;
-  unsigned long long *evals;
+  unsigned long long *stats;  // [0] distance evaluations, [1] top-k insertions (or nullptr)
 };
 
+// per-axis shift class of a (query box, source box) pair: 0 = no wrap for any pair,
+// 1 = every pair wraps by -L, 2 = every pair wraps by +L (shift returned in sh),
+// 3 = straddles (per-pair select)
+__device__ __forceinline__ int shift_class(float qlo, float qhi, float slo, float shi, float L, float h, float &sh) {
+  const float tmin = __fsub_rn(qlo, shi), tmax = __fsub_rn(qhi, slo);
+  sh = 0.f;
+  if (tmin >= h) {
+    sh = -L;
+    return 1;
+  }
+  if (tmax < -h) {
+    sh = L;
+    return 2;
+  }
+  if (tmin >= -h && tmax < h) return 0;
+  return 3;
+}
+
+__device__ __forceinline__ bool any_straddle(int c) {
+  return ((c & 3) == 3) || (((c >> 2) & 3) == 3) || (((c >> 4) & 3) == 3);
+}
+
+struct WarpBuf {
+  float x[kLCap], y[kLCap], z[kLCap];
+  int g[kLCap];
+};
+
+template <int K>
+struct Lane {
+  u64 tk[K];
+  float kth;
+  unsigned ins;
+};
+
+template <int K>
+__device__ __forceinline__ void cand(Lane<K> &L, float d2, int g) {
+  if (d2 <= L.kth) {
+    const u64 key = ((u64)__float_as_uint(d2) << 32) | (unsigned)(g + 1);
+    if (key < L.tk[K - 1]) {
+      topk_insert<K>(L.tk, key);
+      L.kth = __uint_as_float((unsigned)(L.tk[K - 1] >> 32));
+      ++L.ins;
+    }
+  }
+}
+
+// evaluate staged sources [0, n) (n multiple of 4, NaN padded) against the lane's query
+template <int K, bool SHIFT>
+__device__ __forceinline__ void eval_block(const WarpBuf &B, int n, float qx, float qy, float qz, float shx, float shy,
+                                           float shz, Lane<K> &L) {
+  const u64 QX = pk(qx, qx), QY = pk(qy, qy), QZ = pk(qz, qz);
+  const u64 SX = pk(shx, shx), SY = pk(shy, shy), SZ = pk(shz, shz);
+  for (int j = 0; j < n; j += 4) {
+    const float4 X = *reinterpret_cast<const float4 *>(&B.x[j]);
+    const float4 Y = *reinterpret_cast<const float4 *>(&B.y[j]);
+    const float4 Z = *reinterpret_cast<const float4 *>(&B.z[j]);
+    u64 tx0 = sub2(QX, pk(X.x, X.y)), tx1 = sub2(QX, pk(X.z, X.w));
+    u64 ty0 = sub2(QY, pk(Y.x, Y.y)), ty1 = sub2(QY, pk(Y.z, Y.w));
+    u64 tz0 = sub2(QZ, pk(Z.x, Z.y)), tz1 = sub2(QZ, pk(Z.z, Z.w));
+    if (SHIFT) {
+      tx0 = add2(tx0, SX);
+      tx1 = add2(tx1, SX);
+      ty0 = add2(ty0, SY);
+      ty1 = add2(ty1, SY);
+      tz0 = add2(tz0, SZ);
+      tz1 = add2(tz1, SZ);
+    }
+    const u64 d0 = fma2(tz0, tz0, fma2(ty0, ty0, mul2(tx0, tx0)));
+    const u64 d1 = fma2(tz1, tz1, fma2(ty1, ty1, mul2(tx1, tx1)));
+    float a0, a1, a2, a3;
+    upk(d0, a0, a1);
+    upk(d1, a2, a3);
+    const float m = fminf(fminf(a0, a1), fminf(a2, a3));  // NaN padding is ignored by min
+    if (__any_sync(0xffffffffu, m <= L.kth)) {
+      const int4 G = *reinterpret_cast<const int4 *>(&B.g[j]);
+      cand<K>(L, a0, G.x);
+      cand<K>(L, a1, G.y);
+      cand<K>(L, a2, G.z);
+      cand<K>(L, a3, G.w);
+    }
+  }
+}
+
+template <int K>
+__device__ __forceinline__ void eval_generic(const WarpBuf &B, int n, float qx, float qy, float qz, const Dom &D,
+                                             Lane<K> &L) {
+  for (int j = 0; j < n; ++j) {
+    const float d2 = canon_d2_per(qx, qy, qz, B.x[j], B.y[j], B.z[j], D);  // NaN padding -> NaN
+    cand<K>(L, d2, B.g[j]);
+  }
+}
+
 template <int K, bool PER>
-__global__ void __launch_bounds__(kLeafWarps * 32) k_leaf2leaf(LeafK a, Dom D) {
-  extern __shared__ float4 s_pts[];
+__global__ void __launch_bounds__(kLThreads) k_leaf(LeafPK a, Dom D) {
+  __shared__ __align__(16) WarpBuf s_buf[kLWarps];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  float4 *sp = s_pts + warp * a.nmax0;
-  const int64_t item = (int64_t)blockIdx.x * kLeafWarps + warp;
-  const int64_t leaf = item / a.chunks;
-  const int chunk = (int)(item % a.chunks);
-  if (leaf >= a.nleaf) return;
-  const int qb = a.leaf_beg[leaf], qe = a.leaf_beg[leaf + 1];
-  const int q0 = qb + chunk * 32;
-  if (q0 >= qe) return;
-  const int qi = q0 + lane;
-  bool act = qi < qe;
-  float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+  const int64_t item = (int64_t)blockIdx.x * kLWarps + warp;
+  if (item >= a.nitems) return;
+  WarpBuf &B = s_buf[warp];
+  const int J = a.item_par[item];
+  const int qhi = a.leaf_beg[a.par_leaf[J + 1]];
+  const int qi = a.item_q0[item] + lane;
+  bool act = qi < qhi;
+  float qx = 0.f, qy = 0.f, qz = 0.f, qw = 0.f;
   int inpos = 0;
   if (act) {
-    q = a.pts[qi];
+    const float4 q = a.pts[qi];
+    qx = q.x;
+    qy = q.y;
+    qz = q.z;
+    qw = q.w;
     inpos = a.perm[qi];
     act = inpos < a.n_query;
   }
   if (!__any_sync(0xffffffffu, act)) return;
-
-  // top-k: slots [0, K-k) hold 0 (below every real key), [K-k, K) start at the sentinel (R_max^2, max)
-  const float R = a.rmax2[leaf];
-  unsigned long long tk[K];
-  const unsigned long long sentinel = ((unsigned long long)__float_as_uint(R) << 32) | 0xffffffffull;
+  float blo[3] = {act ? qx : INFINITY, act ? qy : INFINITY, act ? qz : INFINITY};
+  float bhi[3] = {act ? qx : -INFINITY, act ? qy : -INFINITY, act ? qz : -INFINITY};
 #pragma unroll
-  for (int j = 0; j < K; ++j) tk[j] = (j < K - a.k) ? 0ull : sentinel;
-  float kth = R;
+  for (int d = 0; d < 3; ++d) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      blo[d] = fminf(blo[d], __shfl_xor_sync(0xffffffffu, blo[d], o));
+      bhi[d] = fmaxf(bhi[d], __shfl_xor_sync(0xffffffffu, bhi[d], o));
+    }
+  }
+  NodeBox wbox;
+  wbox.lo = make_float4(blo[0], blo[1], blo[2], 0.f);
+  wbox.hi = make_float4(bhi[0], bhi[1], bhi[2], 0.f);
 
-  const NodeBox qbox = a.leaf_box[leaf];
-  const int64_t eb = a.ispl[leaf], ee = a.ispl[leaf + 1];
+  const float R0 = a.rmax2 ? a.rmax2[J] : INFINITY;
+  Lane<K> L;
+  {
+    const u64 sentinel = ((u64)__float_as_uint(R0) << 32) | 0xffffffffull;
+#pragma unroll
+    for (int j = 0; j < K; ++j) L.tk[j] = (j < K - a.k) ? 0ull : sentinel;
+    L.kth = act ? R0 : -1.f;  // inactive lanes never pass a comparison
+    L.ins = 0;
+  }
   unsigned long long nev = 0;
+  const int64_t eb = a.ispl[J], ee = a.ispl[J + 1];
   for (int64_t e = eb; e < ee; ++e) {
-    const int s = a.isrc[e];
-    if (a.early) {
-      const float rl = a.rlow[e];
-      const unsigned m = __reduce_max_sync(0xffffffffu, act ? __float_as_uint(kth) : 0u);
-      if (rl > __uint_as_float(m)) {
-        if (a.sorted) break;
-        continue;
-      }
+    const int S = a.isrc[e];
+    const float wmax = a.early ? __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(fmaxf(L.kth, 0.f))))
+                               : INFINITY;
+    if (a.rlow[e] > wmax) {
+      if (a.sorted) break;
+      continue;
     }
-    const int sb = a.leaf_beg[s], se = a.leaf_beg[s + 1];
-    const int m = se - sb;
-    __syncwarp();
-    for (int t = lane; t < m; t += 32) sp[t] = a.pts[sb + t];
-    __syncwarp();
-    // periodic shift classes (uniform over the warp: all lanes share the query leaf)
-    float sh[3] = {0.f, 0.f, 0.f};
-    bool straddle = false, shifted = false;
-    if (PER) {
-      const NodeBox sbx = a.leaf_box[s];
-      const float qlo[3] = {qbox.lo.x, qbox.lo.y, qbox.lo.z}, qhi[3] = {qbox.hi.x, qbox.hi.y, qbox.hi.z};
-      const float slo[3] = {sbx.lo.x, sbx.lo.y, sbx.lo.z}, shi[3] = {sbx.hi.x, sbx.hi.y, sbx.hi.z};
-#pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        const float tmin = __fsub_rn(qlo[d], shi[d]), tmax = __fsub_rn(qhi[d], slo[d]);
-        if (tmin >= D.h[d]) {
-          sh[d] = -D.L[d];
-          shifted = true;
-        } else if (tmax < -D.h[d]) {
-          sh[d] = D.L[d];
-          shifted = true;
-        } else if (!(tmin >= -D.h[d] && tmax < D.h[d])) {
-          straddle = true;
+    if (a.par_box && box_dlow2(wbox, a.par_box[S], D) > wmax) continue;
+    const int la = a.par_leaf[S], lb = a.par_leaf[S + 1];
+    for (int l0 = la; l0 < lb; l0 += 32) {
+      // one lane per child leaf: exact box bound against the warp's queries
+      const int l = l0 + lane;
+      bool pass = false;
+      int cls = 0;
+      if (l < lb) {
+        const NodeBox lbx = a.leaf_box[l];
+        pass = box_dlow2(wbox, lbx, D) <= wmax;
+        if (PER && pass) {
+          float shd;
+          cls |= shift_class(wbox.lo.x, wbox.hi.x, lbx.lo.x, lbx.hi.x, D.L[0], D.h[0], shd) << 0;
+          cls |= shift_class(wbox.lo.y, wbox.hi.y, lbx.lo.y, lbx.hi.y, D.L[1], D.h[1], shd) << 2;
+          cls |= shift_class(wbox.lo.z, wbox.hi.z, lbx.lo.z, lbx.hi.z, D.L[2], D.h[2], shd) << 4;
         }
       }
-    }
-    if (act) {
-      nev += (unsigned)m;
-      if (!PER || (!straddle && !shifted)) {
-        for (int j = 0; j < m; ++j) {
-          const float4 sv = sp[j];
-          const float d2 = canon_d2_open(q.x, q.y, q.z, sv.x, sv.y, sv.z);
-          if (d2 <= kth) {
-            const unsigned long long key =
-                ((unsigned long long)__float_as_uint(d2) << 32) | (unsigned)(__float_as_int(sv.w) + 1);
-            if (key < tk[K - 1]) {
-              topk_insert<K>(tk, key);
-              kth = __uint_as_float((unsigned)(tk[K - 1] >> 32));
-            }
+      unsigned bal = __ballot_sync(0xffffffffu, pass);
+      while (bal) {
+        // batch consecutive surviving leaves of one shift class into the warp buffer
+        const int first = __ffs(bal) - 1;
+        const int c0 = __shfl_sync(0xffffffffu, cls, first);
+        int n = 0;
+        while (bal) {
+          const int src = __ffs(bal) - 1;
+          if (__shfl_sync(0xffffffffu, cls, src) != c0) break;
+          const int lp = a.leaf_beg[l0 + src], m = a.leaf_beg[l0 + src + 1] - lp;
+          if (n + ((m + 3) & ~3) > kLCap) break;
+          bal &= bal - 1;
+          for (int t = lane; t < ((m + 3) & ~3); t += 32) {
+            float4 p = make_float4(__int_as_float(0x7fc00000), __int_as_float(0x7fc00000),
+                                   __int_as_float(0x7fc00000), 0.f);
+            if (t < m) p = a.pts[lp + t];
+            B.x[n + t] = p.x;
+            B.y[n + t] = p.y;
+            B.z[n + t] = p.z;
+            B.g[n + t] = __float_as_int(p.w);
           }
+          nev += act ? (unsigned)m : 0u;
+          n += (m + 3) & ~3;
         }
-      } else if (!straddle) {
-        for (int j = 0; j < m; ++j) {
-          const float4 sv = sp[j];
-          const float tx = __fadd_rn(__fsub_rn(q.x, sv.x), sh[0]);
-          const float ty = __fadd_rn(__fsub_rn(q.y, sv.y), sh[1]);
-          const float tz = __fadd_rn(__fsub_rn(q.z, sv.z), sh[2]);
-          const float d2 = __fmaf_rn(tz, tz, __fmaf_rn(ty, ty, __fmul_rn(tx, tx)));
-          if (d2 <= kth) {
-            const unsigned long long key =
-                ((unsigned long long)__float_as_uint(d2) << 32) | (unsigned)(__float_as_int(sv.w) + 1);
-            if (key < tk[K - 1]) {
-              topk_insert<K>(tk, key);
-              kth = __uint_as_float((unsigned)(tk[K - 1] >> 32));
-            }
-          }
+        __syncwarp();
+        if (!PER || c0 == 0) {
+          eval_block<K, false>(B, n, qx, qy, qz, 0.f, 0.f, 0.f, L);
+        } else if (!any_straddle(c0)) {  // no axis straddles: uniform exact shift
+          float s0, s1, s2;
+          const NodeBox lbx = a.leaf_box[l0 + first];
+          shift_class(wbox.lo.x, wbox.hi.x, lbx.lo.x, lbx.hi.x, D.L[0], D.h[0], s0);
+          shift_class(wbox.lo.y, wbox.hi.y, lbx.lo.y, lbx.hi.y, D.L[1], D.h[1], s1);
+          shift_class(wbox.lo.z, wbox.hi.z, lbx.lo.z, lbx.hi.z, D.L[2], D.h[2], s2);
+          eval_block<K, true>(B, n, qx, qy, qz, s0, s1, s2, L);
+        } else {
+          eval_generic<K>(B, n, qx, qy, qz, D, L);
         }
-      } else {
-        for (int j = 0; j < m; ++j) {
-          const float4 sv = sp[j];
-          const float d2 = canon_d2_per(q.x, q.y, q.z, sv.x, sv.y, sv.z, D);
-          if (d2 <= kth) {
-            const unsigned long long key =
-                ((unsigned long long)__float_as_uint(d2) << 32) | (unsigned)(__float_as_int(sv.w) + 1);
-            if (key < tk[K - 1]) {
-              topk_insert<K>(tk, key);
-              kth = __uint_as_float((unsigned)(tk[K - 1] >> 32));
-            }
-          }
-        }
+        __syncwarp();
       }
     }
   }
-  if (a.evals) {
-    unsigned long long tot = nev;
+  if (a.stats) {
+    unsigned long long tot = nev, ins = L.ins;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-    if (lane == 0 && tot) atomicAdd(a.evals, tot);
+    for (int o = 16; o > 0; o >>= 1) {
+      tot += __shfl_xor_sync(0xffffffffu, tot, o);
+      ins += __shfl_xor_sync(0xffffffffu, ins, o);
+    }
+    if (lane == 0) {
+      atomicAdd(&a.stats[0], tot);
+      atomicAdd(&a.stats[1], ins);
+    }
   }
   if (act) {
     const int64_t row = a.order == JZ_ORDER_INPUT ? (int64_t)inpos : (a.zrow ? (int64_t)a.zrow[qi] : (int64_t)qi);
@@ -186,51 +322,93 @@ __global__ void __launch_bounds__(kLeafWarps * 32) k_leaf2leaf(LeafK a, Dom D) {
 #pragma unroll
     for (int j = 0; j < K; ++j) {
       if (j >= K - a.k) {
-        oi[j - (K - a.k)] = (int32_t)((unsigned)(tk[j] & 0xffffffffu) - 1u);
-        od[j - (K - a.k)] = __uint_as_float((unsigned)(tk[j] >> 32));
+        oi[j - (K - a.k)] = (int32_t)((unsigned)(L.tk[j] & 0xffffffffu) - 1u);
+        od[j - (K - a.k)] = __uint_as_float((unsigned)(L.tk[j] >> 32));
       }
     }
-    if (a.out_row_gidx) a.out_row_gidx[row] = __float_as_int(q.w);
+    if (a.out_row_gidx) a.out_row_gidx[row] = __float_as_int(qw);
+  }
+}
+
+// work items: 32-query groups of each receiving parent, in z order
+__global__ void k_item_count(const int32_t *__restrict__ par_leaf, const int32_t *__restrict__ leaf_beg, int64_t npar,
+                             int32_t *__restrict__ cnt) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < npar; j += (int64_t)gridDim.x * blockDim.x) {
+    const int n = leaf_beg[par_leaf[j + 1]] - leaf_beg[par_leaf[j]];
+    cnt[j] = (n + 31) >> 5;
+  }
+}
+
+__global__ void k_item_fill(const int32_t *__restrict__ par_leaf, const int32_t *__restrict__ leaf_beg, int64_t npar,
+                            const int64_t *__restrict__ off, int32_t *__restrict__ item_par,
+                            int32_t *__restrict__ item_q0) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < npar; j += (int64_t)gridDim.x * blockDim.x) {
+    const int q0 = leaf_beg[par_leaf[j]], q1 = leaf_beg[par_leaf[j + 1]];
+    int64_t o = off[j];
+    for (int q = q0; q < q1; q += 32, ++o) {
+      item_par[o] = (int32_t)j;
+      item_q0[o] = q;
+    }
   }
 }
 
 template <int K>
-static void launch_k(const LeafK &la, const Dom &D, unsigned blocks, size_t smem, cudaStream_t st) {
-  if (D.periodic) k_leaf2leaf<K, true><<<blocks, kLeafWarps * 32, smem, st>>>(la, D);
-  else k_leaf2leaf<K, false><<<blocks, kLeafWarps * 32, smem, st>>>(la, D);
+static void launch_l(const LeafPK &la, const Dom &D, unsigned blocks, cudaStream_t st) {
+  if (D.periodic) k_leaf<K, true><<<blocks, kLThreads, 0, st>>>(la, D);
+  else k_leaf<K, false><<<blocks, kLThreads, 0, st>>>(la, D);
 }
 
 void leaf_to_leaf(const LeafArgs &a, const Dom &D, cudaStream_t st) {
-  LeafK la;
+  if (a.npar == 0) return;
+  int32_t *cnt = nullptr;
+  int64_t *off = nullptr;
+  JZ_CUDA(cudaMallocAsync(&cnt, a.npar * sizeof(int32_t), st));
+  JZ_CUDA(cudaMallocAsync(&off, (a.npar + 1) * sizeof(int64_t), st));
+  k_item_count<<<grid_for(a.npar, 256), 256, 0, st>>>(a.par_leaf, a.leaf_beg, a.npar, cnt);
+  JZ_LAUNCH_CHECK();
+  exclusive_scan_i32_to_i64(cnt, off, a.npar, st);
+  const int64_t nitems = read_i64(off + a.npar, st);
+  int32_t *item_par = nullptr, *item_q0 = nullptr;
+  JZ_CUDA(cudaMallocAsync(&item_par, (nitems + 1) * sizeof(int32_t), st));
+  JZ_CUDA(cudaMallocAsync(&item_q0, (nitems + 1) * sizeof(int32_t), st));
+  k_item_fill<<<grid_for(a.npar, 256), 256, 0, st>>>(a.par_leaf, a.leaf_beg, a.npar, off, item_par, item_q0);
+  JZ_LAUNCH_CHECK();
+
+  LeafPK la;
   la.pts = a.pts;
   la.leaf_beg = a.leaf_beg;
   la.leaf_box = a.leaf_box;
+  la.par_leaf = a.par_leaf;
+  la.par_box = a.par_box;
   la.ispl = a.il->ispl;
   la.isrc = a.il->isrc;
   la.rlow = a.il->rlow;
   la.rmax2 = a.rmax2;
+  la.item_par = item_par;
+  la.item_q0 = item_q0;
+  la.nitems = nitems;
   la.perm = a.perm;
   la.zrow = a.zrow;
-  la.nleaf = a.nleaf;
   la.n_query = a.n_query;
   la.k = a.k;
   la.order = a.order;
-  la.nmax0 = a.nmax0;
-  la.chunks = (int)ceil_div(a.nmax0, 32);
   la.early = !(a.flags & JZ_FLAG_NO_EARLY_EXIT);
-  la.sorted = !(a.flags & JZ_FLAG_NO_SEGSORT);
+  la.sorted = !(a.flags & (JZ_FLAG_NO_SEGSORT | JZ_FLAG_NO_EARLY_EXIT));
   la.out_idx = a.out_idx;
   la.out_d2 = a.out_d2;
   la.out_row_gidx = a.out_row_gidx;
-  la.evals = a.evals;
-  const int64_t items = a.nleaf * la.chunks;
-  const unsigned blocks = (unsigned)ceil_div(items, kLeafWarps);
-  const size_t smem = (size_t)kLeafWarps * a.nmax0 * sizeof(float4);
-  if (blocks == 0) return;
-  if (a.k <= 8) launch_k<8>(la, D, blocks, smem, st);
-  else if (a.k <= 16) launch_k<16>(la, D, blocks, smem, st);
-  else launch_k<32>(la, D, blocks, smem, st);
-  JZ_LAUNCH_CHECK();
+  la.stats = a.evals;
+  const unsigned blocks = (unsigned)ceil_div(nitems, kLWarps);
+  if (blocks) {
+    if (a.k <= 8) launch_l<8>(la, D, blocks, st);
+    else if (a.k <= 16) launch_l<16>(la, D, blocks, st);
+    else launch_l<32>(la, D, blocks, st);
+    JZ_LAUNCH_CHECK();
+  }
+  JZ_CUDA(cudaFreeAsync(cnt, st));
+  JZ_CUDA(cudaFreeAsync(off, st));
+  JZ_CUDA(cudaFreeAsync(item_par, st));
+  JZ_CUDA(cudaFreeAsync(item_q0, st));
 }
 
 }  // namespace jz

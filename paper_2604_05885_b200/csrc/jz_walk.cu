@@ -250,8 +250,8 @@ __global__ void __launch_bounds__(kSegWarps * 32) k_segsort(const int64_t *__res
   }
 }
 
-void walk_to_leaves(const std::vector<Plane> &planes, const Dom &D, int k, int ngr, unsigned flags, IList &leaf_il,
-                    float **rmax2_leaf, cudaStream_t st) {
+void walk_to(const std::vector<Plane> &planes, const Dom &D, int k, int ngr, unsigned flags, int stop, IList &out_il,
+             float **rmax2_out, int32_t **superbeg_out, cudaStream_t st) {
   const int P = (int)planes.size();
   const int top = P - 1;
   const int64_t ntop = planes[top].nnodes;
@@ -270,12 +270,13 @@ void walk_to_leaves(const std::vector<Plane> &planes, const Dom &D, int k, int n
   JZ_CUDA(cudaMallocAsync(&il.rlow, il.total * sizeof(float), st));
   k_dense_init<<<grid_for(S * S + 2, 256), 256, 0, st>>>(S, il.ispl, il.isrc, il.rlow);
   JZ_LAUNCH_CHECK();
-  for (int p = top; p >= 0; --p) {
+  float *rmax2 = nullptr;
+  for (int p = top; p >= stop; --p) {
     const int32_t *pbeg = (p == top) ? superbeg : planes[p + 1].beg;
     const int64_t npar = (p == top) ? S : planes[p + 1].nnodes;
     const Plane &pl = planes[p];
-    float *rmax2 = nullptr;
     int32_t *cnt = nullptr;
+    if (rmax2) JZ_CUDA(cudaFreeAsync(rmax2, st));
     JZ_CUDA(cudaMallocAsync(&rmax2, pl.nnodes * sizeof(float), st));
     JZ_CUDA(cudaMallocAsync(&cnt, pl.nnodes * sizeof(int32_t), st));
     const int srt = do_sort ? 1 : 0;
@@ -304,11 +305,15 @@ void walk_to_leaves(const std::vector<Plane> &planes, const Dom &D, int k, int n
     il.release(st);
     il = nl;
     JZ_CUDA(cudaFreeAsync(cnt, st));
-    if (p > 0) JZ_CUDA(cudaFreeAsync(rmax2, st));
-    else *rmax2_leaf = rmax2;
   }
-  JZ_CUDA(cudaFreeAsync(superbeg, st));
-  leaf_il = il;
+  out_il = il;
+  *rmax2_out = rmax2;
+  if (stop > top) {
+    *superbeg_out = superbeg;
+  } else {
+    JZ_CUDA(cudaFreeAsync(superbeg, st));
+    *superbeg_out = nullptr;
+  }
 }
 
 }  // namespace jz
