@@ -107,6 +107,14 @@ __device__ __forceinline__ float box_dup2(const NodeBox &a, const NodeBox &b, co
   return __fmaf_rn(uz, uz, __fmaf_rn(uy, uy, __fmul_rn(ux, ux)));
 }
 
+// point-to-box lower bound: min over s in [lo, hi] of the canonical d2(q, s) (exact, as above)
+__device__ __forceinline__ float pt_box_dlow2(float qx, float qy, float qz, const NodeBox &b, const Dom &D) {
+  float gx = axis_low(qx, qx, b.lo.x, b.hi.x, D.periodic, D.L[0], D.h[0]);
+  float gy = axis_low(qy, qy, b.lo.y, b.hi.y, D.periodic, D.L[1], D.h[1]);
+  float gz = axis_low(qz, qz, b.lo.z, b.hi.z, D.periodic, D.L[2], D.h[2]);
+  return __fmaf_rn(gz, gz, __fmaf_rn(gy, gy, __fmul_rn(gx, gx)));
+}
+
 __device__ __forceinline__ int box_count(const NodeBox &b) { return __float_as_int(b.lo.w); }
 
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }

@@ -28,6 +28,7 @@ namespace jz {
 constexpr int kLWarps = 4;
 constexpr int kLThreads = kLWarps * 32;
 constexpr int kLCap = 256;  // staged source points per warp (4 KB SoA)
+constexpr int kQCap = 16;   // per-lane candidate queue (4 KB per warp)
 
 typedef unsigned long long u64;
 
@@ -60,15 +61,22 @@ __device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c) {
   return d;
 }
 
+// Sorted insert of `key` (known to be < a[K-1]) into a[0..K). The list is cut into quarters;
+// a quarter is touched only if key < its last element, so the common late insertion near the
+// tail costs one quarter of the compare/select network.
 template <int K>
 __device__ __forceinline__ void topk_insert(u64 (&a)[K], u64 key) {
+  constexpr int Q = K / 4;
 #pragma unroll
-  for (int j = K - 1; j > 0; --j) {
-    const bool mv = key < a[j - 1];
-    const bool here = !mv && key < a[j];
-    a[j] = mv ? a[j - 1] : (here ? key : a[j]);
+  for (int q = 3; q >= 0; --q) {
+    if (key < a[q * Q + Q - 1]) {
+#pragma unroll
+      for (int j = q * Q + Q - 1; j >= q * Q; --j) {
+        const bool mv = j > 0 && key < a[j > 0 ? j - 1 : 0];
+        a[j] = mv ? a[j > 0 ? j - 1 : 0] : (key < a[j] ? key : a[j]);
+      }
+    }
   }
-  if (key < a[0]) a[0] = key;
 }
 
 struct LeafPK {
@@ -122,6 +130,7 @@ __device__ __forceinline__ bool any_straddle(int c) {
 struct WarpBuf {
   float x[kLCap], y[kLCap], z[kLCap];
   int g[kLCap];
+  u64 q[kQCap][32];  // candidate queue, lane-minor
 };
 
 template <int K>
@@ -129,7 +138,28 @@ struct Lane {
   u64 tk[K];
   float kth;
   unsigned ins;
+  int qn;    // queued candidates
+  bool act;  // lane holds a query (inactive lanes keep kth = -1)
 };
+
+// Insert the lane's queued candidates: all lanes drain their queues in parallel, so the
+// warp runs max(queue length) insertion rounds instead of one per candidate group.
+template <int K>
+__device__ __forceinline__ void flush(WarpBuf &B, Lane<K> &L) {
+  const int lane = threadIdx.x & 31;
+  const int mx = __reduce_max_sync(0xffffffffu, (unsigned)L.qn);
+  for (int i = 0; i < mx; ++i) {
+    if (i < L.qn) {
+      const u64 key = B.q[i][lane];
+      if (key < L.tk[K - 1]) {
+        topk_insert<K>(L.tk, key);
+        ++L.ins;
+      }
+    }
+  }
+  L.kth = L.act ? __uint_as_float((unsigned)(L.tk[K - 1] >> 32)) : -1.f;
+  L.qn = 0;
+}
 
 template <int K>
 __device__ __forceinline__ void cand(Lane<K> &L, float d2, int g) {
@@ -143,9 +173,17 @@ __device__ __forceinline__ void cand(Lane<K> &L, float d2, int g) {
   }
 }
 
+template <int K>
+__device__ __forceinline__ void enqueue(WarpBuf &B, Lane<K> &L, float d2, int g) {
+  if (d2 <= L.kth) {
+    B.q[L.qn][threadIdx.x & 31] = ((u64)__float_as_uint(d2) << 32) | (unsigned)(g + 1);
+    ++L.qn;
+  }
+}
+
 // evaluate staged sources [0, n) (n multiple of 4, NaN padded) against the lane's query
 template <int K, bool SHIFT>
-__device__ __forceinline__ void eval_block(const WarpBuf &B, int n, float qx, float qy, float qz, float shx, float shy,
+__device__ __forceinline__ void eval_block(WarpBuf &B, int n, float qx, float qy, float qz, float shx, float shy,
                                            float shz, Lane<K> &L) {
   const u64 QX = pk(qx, qx), QY = pk(qy, qy), QZ = pk(qz, qz);
   const u64 SX = pk(shx, shx), SY = pk(shy, shy), SZ = pk(shz, shz);
@@ -172,12 +210,14 @@ __device__ __forceinline__ void eval_block(const WarpBuf &B, int n, float qx, fl
     const float m = fminf(fminf(a0, a1), fminf(a2, a3));  // NaN padding is ignored by min
     if (__any_sync(0xffffffffu, m <= L.kth)) {
       const int4 G = *reinterpret_cast<const int4 *>(&B.g[j]);
-      cand<K>(L, a0, G.x);
-      cand<K>(L, a1, G.y);
-      cand<K>(L, a2, G.z);
-      cand<K>(L, a3, G.w);
+      enqueue<K>(B, L, a0, G.x);
+      enqueue<K>(B, L, a1, G.y);
+      enqueue<K>(B, L, a2, G.z);
+      enqueue<K>(B, L, a3, G.w);
+      if (__any_sync(0xffffffffu, L.qn > kQCap - 4)) flush<K>(B, L);
     }
   }
+  if (__any_sync(0xffffffffu, L.qn > 0)) flush<K>(B, L);
 }
 
 template <int K>
@@ -189,6 +229,85 @@ __device__ __forceinline__ void eval_generic(const WarpBuf &B, int n, float qx, 
   }
 }
 
+// Visit the child leaves [la, lb) of one source node, skipping [xa, xb): one lane tests one
+// leaf (exact box bound vs the warp's current max k-th distance), then every lane tests its own
+// query against each surviving leaf (skip unless some lane needs it); survivors are staged in
+// batches of one periodic shift class and evaluated.
+template <int K, bool PER>
+__device__ __forceinline__ void visit_leaves(const LeafPK &a, const Dom &D, WarpBuf &B, const NodeBox &wbox, float wmax,
+                                             int la, int lb, int xa, int xb, float qx, float qy, float qz, bool act,
+                                             Lane<K> &L, unsigned long long &nev) {
+  const int lane = threadIdx.x & 31;
+  for (int l0 = la; l0 < lb; l0 += 32) {
+    const int l = l0 + lane;
+    bool pass = false;
+    int cls = 0;
+    if (l < lb && (l < xa || l >= xb)) {
+      const NodeBox lbx = a.leaf_box[l];
+      pass = box_dlow2(wbox, lbx, D) <= wmax;
+      if (PER && pass) {
+        float shd;
+        cls |= shift_class(wbox.lo.x, wbox.hi.x, lbx.lo.x, lbx.hi.x, D.L[0], D.h[0], shd) << 0;
+        cls |= shift_class(wbox.lo.y, wbox.hi.y, lbx.lo.y, lbx.hi.y, D.L[1], D.h[1], shd) << 2;
+        cls |= shift_class(wbox.lo.z, wbox.hi.z, lbx.lo.z, lbx.hi.z, D.L[2], D.h[2], shd) << 4;
+      }
+    }
+    unsigned bal = __ballot_sync(0xffffffffu, pass);
+    while (bal) {
+      // batch consecutive surviving leaves of one shift class into the warp buffer
+      const int first = __ffs(bal) - 1;
+      const int c0 = __shfl_sync(0xffffffffu, cls, first);
+      int n = 0;
+      while (bal) {
+        const int src = __ffs(bal) - 1;
+        if (__shfl_sync(0xffffffffu, cls, src) != c0) break;
+        // per-lane test: does any lane's query reach this leaf within its own k-th distance?
+        {
+          const NodeBox lbx = a.leaf_box[l0 + src];
+          const bool need = L.act && pt_box_dlow2(qx, qy, qz, lbx, D) <= L.kth;
+          if (!__any_sync(0xffffffffu, need)) {
+            bal &= bal - 1;
+            continue;
+          }
+        }
+        const int lp = a.leaf_beg[l0 + src], m = a.leaf_beg[l0 + src + 1] - lp;
+        if (n + ((m + 3) & ~3) > kLCap) break;
+        bal &= bal - 1;
+        for (int t = lane; t < ((m + 3) & ~3); t += 32) {
+          float4 p = make_float4(__int_as_float(0x7fc00000), __int_as_float(0x7fc00000), __int_as_float(0x7fc00000),
+                                 0.f);
+          if (t < m) p = a.pts[lp + t];
+          B.x[n + t] = p.x;
+          B.y[n + t] = p.y;
+          B.z[n + t] = p.z;
+          B.g[n + t] = __float_as_int(p.w);
+        }
+        nev += act ? (unsigned)m : 0u;
+        n += (m + 3) & ~3;
+      }
+      __syncwarp();
+      if (n == 0) continue;
+      if (!PER || c0 == 0) {
+        eval_block<K, false>(B, n, qx, qy, qz, 0.f, 0.f, 0.f, L);
+      } else if (!any_straddle(c0)) {  // no axis straddles: uniform exact shift
+        float s0, s1, s2;
+        const NodeBox lbx = a.leaf_box[l0 + first];
+        shift_class(wbox.lo.x, wbox.hi.x, lbx.lo.x, lbx.hi.x, D.L[0], D.h[0], s0);
+        shift_class(wbox.lo.y, wbox.hi.y, lbx.lo.y, lbx.hi.y, D.L[1], D.h[1], s1);
+        shift_class(wbox.lo.z, wbox.hi.z, lbx.lo.z, lbx.hi.z, D.L[2], D.h[2], s2);
+        eval_block<K, true>(B, n, qx, qy, qz, s0, s1, s2, L);
+      } else {
+        eval_generic<K>(B, n, qx, qy, qz, D, L);
+      }
+      __syncwarp();
+    }
+  }
+}
+
+__device__ __forceinline__ float warp_max_kth(float kth) {
+  return __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(fmaxf(kth, 0.f))));
+}
+
 template <int K, bool PER>
 __global__ void __launch_bounds__(kLThreads) k_leaf(LeafPK a, Dom D) {
   __shared__ __align__(16) WarpBuf s_buf[kLWarps];
@@ -197,8 +316,10 @@ __global__ void __launch_bounds__(kLThreads) k_leaf(LeafPK a, Dom D) {
   if (item >= a.nitems) return;
   WarpBuf &B = s_buf[warp];
   const int J = a.item_par[item];
-  const int qhi = a.leaf_beg[a.par_leaf[J + 1]];
-  const int qi = a.item_q0[item] + lane;
+  const int LJa = a.par_leaf[J], LJb = a.par_leaf[J + 1];
+  const int qhi = a.leaf_beg[LJb];
+  const int q0 = a.item_q0[item];
+  const int qi = q0 + lane;
   bool act = qi < qhi;
   float qx = 0.f, qy = 0.f, qz = 0.f, qw = 0.f;
   int inpos = 0;
@@ -234,74 +355,36 @@ __global__ void __launch_bounds__(kLThreads) k_leaf(LeafPK a, Dom D) {
     for (int j = 0; j < K; ++j) L.tk[j] = (j < K - a.k) ? 0ull : sentinel;
     L.kth = act ? R0 : -1.f;  // inactive lanes never pass a comparison
     L.ins = 0;
+    L.qn = 0;
+    L.act = act;
   }
   unsigned long long nev = 0;
+  // pre-pass: the leaves holding the warp's own queries (tightens the k-th bound early)
+  int xa = 0x7fffffff, xb = -1;
+  {
+    const int qend = min(q0 + 32, qhi);
+    for (int l0 = LJa; l0 < LJb; l0 += 32) {
+      const int l = l0 + lane;
+      const bool ov = l < LJb && a.leaf_beg[l] < qend && a.leaf_beg[l + 1] > q0;
+      const unsigned b = __ballot_sync(0xffffffffu, ov);
+      if (b) {
+        xa = min(xa, l0 + __ffs(b) - 1);
+        xb = max(xb, l0 + 32 - __clz(b));
+      }
+    }
+    visit_leaves<K, PER>(a, D, B, wbox, INFINITY, xa, xb, 0, 0, qx, qy, qz, act, L, nev);
+  }
   const int64_t eb = a.ispl[J], ee = a.ispl[J + 1];
   for (int64_t e = eb; e < ee; ++e) {
     const int S = a.isrc[e];
-    const float wmax = a.early ? __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(fmaxf(L.kth, 0.f))))
-                               : INFINITY;
+    const float wmax = a.early ? warp_max_kth(L.kth) : INFINITY;
     if (a.rlow[e] > wmax) {
       if (a.sorted) break;
       continue;
     }
     if (a.par_box && box_dlow2(wbox, a.par_box[S], D) > wmax) continue;
-    const int la = a.par_leaf[S], lb = a.par_leaf[S + 1];
-    for (int l0 = la; l0 < lb; l0 += 32) {
-      // one lane per child leaf: exact box bound against the warp's queries
-      const int l = l0 + lane;
-      bool pass = false;
-      int cls = 0;
-      if (l < lb) {
-        const NodeBox lbx = a.leaf_box[l];
-        pass = box_dlow2(wbox, lbx, D) <= wmax;
-        if (PER && pass) {
-          float shd;
-          cls |= shift_class(wbox.lo.x, wbox.hi.x, lbx.lo.x, lbx.hi.x, D.L[0], D.h[0], shd) << 0;
-          cls |= shift_class(wbox.lo.y, wbox.hi.y, lbx.lo.y, lbx.hi.y, D.L[1], D.h[1], shd) << 2;
-          cls |= shift_class(wbox.lo.z, wbox.hi.z, lbx.lo.z, lbx.hi.z, D.L[2], D.h[2], shd) << 4;
-        }
-      }
-      unsigned bal = __ballot_sync(0xffffffffu, pass);
-      while (bal) {
-        // batch consecutive surviving leaves of one shift class into the warp buffer
-        const int first = __ffs(bal) - 1;
-        const int c0 = __shfl_sync(0xffffffffu, cls, first);
-        int n = 0;
-        while (bal) {
-          const int src = __ffs(bal) - 1;
-          if (__shfl_sync(0xffffffffu, cls, src) != c0) break;
-          const int lp = a.leaf_beg[l0 + src], m = a.leaf_beg[l0 + src + 1] - lp;
-          if (n + ((m + 3) & ~3) > kLCap) break;
-          bal &= bal - 1;
-          for (int t = lane; t < ((m + 3) & ~3); t += 32) {
-            float4 p = make_float4(__int_as_float(0x7fc00000), __int_as_float(0x7fc00000),
-                                   __int_as_float(0x7fc00000), 0.f);
-            if (t < m) p = a.pts[lp + t];
-            B.x[n + t] = p.x;
-            B.y[n + t] = p.y;
-            B.z[n + t] = p.z;
-            B.g[n + t] = __float_as_int(p.w);
-          }
-          nev += act ? (unsigned)m : 0u;
-          n += (m + 3) & ~3;
-        }
-        __syncwarp();
-        if (!PER || c0 == 0) {
-          eval_block<K, false>(B, n, qx, qy, qz, 0.f, 0.f, 0.f, L);
-        } else if (!any_straddle(c0)) {  // no axis straddles: uniform exact shift
-          float s0, s1, s2;
-          const NodeBox lbx = a.leaf_box[l0 + first];
-          shift_class(wbox.lo.x, wbox.hi.x, lbx.lo.x, lbx.hi.x, D.L[0], D.h[0], s0);
-          shift_class(wbox.lo.y, wbox.hi.y, lbx.lo.y, lbx.hi.y, D.L[1], D.h[1], s1);
-          shift_class(wbox.lo.z, wbox.hi.z, lbx.lo.z, lbx.hi.z, D.L[2], D.h[2], s2);
-          eval_block<K, true>(B, n, qx, qy, qz, s0, s1, s2, L);
-        } else {
-          eval_generic<K>(B, n, qx, qy, qz, D, L);
-        }
-        __syncwarp();
-      }
-    }
+    visit_leaves<K, PER>(a, D, B, wbox, wmax, a.par_leaf[S], a.par_leaf[S + 1], S == J ? xa : 0, S == J ? xb : 0, qx,
+                         qy, qz, act, L, nev);
   }
   if (a.stats) {
     unsigned long long tot = nev, ins = L.ins;
