@@ -214,6 +214,7 @@ def run_single(args):
                        "distribution": c["kind"], "order": "input",
                        "l2": "inputs (1.2 GB positions, 12.8 GB outputs) exceed the 126 MB L2; no flush"},
             "roofline": roofline, "stages_ms": st_ms, "dominant_stage": dominant, "evals_per_query": evals / n, "inserts_per_query": inserts / n,
+            "walk_per_item": {kk: v / max(1, stages[-1]["walk"]["items"]) for kk, v in stages[-1]["walk"].items()},
             "gpu_launches": int(launches * args.steps), "clocks": clocks}
     if not args.profile and not args.no_e2e:
         line["e2e"] = run_e2e(args, pos, box, k)

@@ -135,9 +135,11 @@ JZ_API int jz_knn_search_host(const float *pos_host, int64_t n, const float *box
 JZ_API int jz_knn_stage_times(const jz_knn_index *ix, float out_ms[6], int64_t *evals);
 JZ_API void jz_set_timing(int on);
 
-/* Counters of the last query (host out[4]): [0] distance evaluations, [1] top-k insertions,
- * [2] number of leaves, [3] number of tree planes. */
-JZ_API int jz_knn_stats(const jz_knn_index *ix, int64_t out[4]);
+/* Counters of the last query (host out[9]): [0] distance evaluations, [1] top-k insertions,
+ * [2] number of leaves, [3] number of tree planes, LeafToLeaf walk: [4] interaction entries
+ * visited, [5] leaves passing the warp box test, [6] leaves staged, [7] insertion rounds,
+ * [8] 32-query work items. */
+JZ_API int jz_knn_stats(const jz_knn_index *ix, int64_t out[9]);
 
 /* Number of kernels this library has launched in the process so far. */
 JZ_API int64_t jz_launch_count(void);

@@ -81,9 +81,10 @@ class KnnIndex:
         names = ["frame", "sort", "tree", "node2node", "leaf2leaf", "total"]
         d = {n: float(v) for n, v in zip(names, t)}
         d["evals"] = ev.value
-        st = (ctypes.c_int64 * 4)()
+        st = (ctypes.c_int64 * 9)()
         B.check(self._lib.jz_knn_stats(self._h, st))
         d["inserts"], d["leaves"], d["planes"] = st[1], st[2], st[3]
+        d["walk"] = {"entries": st[4], "leaves_warp": st[5], "leaves_staged": st[6], "rounds": st[7], "items": st[8]}
         return d
 
     # ---- introspection (tests)

@@ -27,6 +27,7 @@ struct jz_knn_index {
   bool timing = false;
   float times[6] = {0, 0, 0, 0, 0, 0};
   long long evals = 0, inserts = 0;
+  long long walk[5] = {0, 0, 0, 0, 0};  // entries, warp-passed leaves, staged leaves, flush rounds, work items
   unsigned long long *d_evals = nullptr;
 };
 
@@ -235,8 +236,8 @@ int jz_knn_query(jz_knn_index *ix, int k, int order, int32_t *out_idx, float *ou
   // walk down to plane 1: its nodes are the receiving parents of LeafToLeaf (jz_leaf.cu)
   jz::walk_to(ix->planes, ix->D, k, ix->prm.ngr, ix->prm.flags, 1, il, &rmax2, &superbeg, st);
   rec(ix, 5);
-  if (!ix->d_evals) JZ_CUDA(cudaMallocAsync(&ix->d_evals, 2 * sizeof(unsigned long long), st));
-  JZ_CUDA(cudaMemsetAsync(ix->d_evals, 0, 2 * sizeof(unsigned long long), st));
+  if (!ix->d_evals) JZ_CUDA(cudaMallocAsync(&ix->d_evals, 16 * sizeof(unsigned long long), st));
+  JZ_CUDA(cudaMemsetAsync(ix->d_evals, 0, 16 * sizeof(unsigned long long), st));
   const bool one_plane = ix->planes.size() == 1;
   jz::LeafArgs la;
   la.pts = ix->pts;
@@ -262,11 +263,13 @@ int jz_knn_query(jz_knn_index *ix, int k, int order, int32_t *out_idx, float *ou
   il.release(st);
   if (rmax2) JZ_CUDA(cudaFreeAsync(rmax2, st));
   if (superbeg) JZ_CUDA(cudaFreeAsync(superbeg, st));
-  unsigned long long ev[2] = {0, 0};
+  unsigned long long ev[16] = {};
   JZ_CUDA(cudaMemcpyAsync(ev, ix->d_evals, sizeof(ev), cudaMemcpyDeviceToHost, st));
   JZ_CUDA(cudaStreamSynchronize(st));
   ix->evals = (long long)ev[0];
   ix->inserts = (long long)ev[1];
+  for (int i = 0; i < 5; ++i) ix->walk[i] = (long long)ev[2 + i];
+
   if (ix->timing) {
     cudaEventElapsedTime(&ix->times[3], ix->ev[4], ix->ev[5]);
     cudaEventElapsedTime(&ix->times[4], ix->ev[5], ix->ev[6]);
@@ -326,12 +329,13 @@ int jz_knn_search_host(const float *pos_host, int64_t n, const float *box, const
   JZ_API_END
 }
 
-int jz_knn_stats(const jz_knn_index *ix, int64_t out[4]) {
+int jz_knn_stats(const jz_knn_index *ix, int64_t out[9]) {
   if (!ix || !out) return fail(JZ_EINVAL, "NULL argument");
   out[0] = ix->evals;
   out[1] = ix->inserts;
   out[2] = ix->planes.empty() ? 0 : ix->planes[0].nnodes;
   out[3] = (int64_t)ix->planes.size();
+  for (int i = 0; i < 5; ++i) out[4 + i] = ix->walk[i];
   return JZ_OK;
 }
 
