@@ -1,0 +1,120 @@
+"""CPU stand-in for the per-rank GPU stages of paper_2604_05885_b200.dist (TEST ONLY).
+
+It lets the real multi-GPU orchestration (dist_knn: splitters, bucketing, count exchange,
+all-to-all-v, query boxes, ghost protocol, z-order rows) run over torch.distributed/gloo on
+CPU. Every stage is a plain numpy / oracle computation; the final per-rank kNN is the oracle's
+brute force over local + ghost points, so the gathered result equals the global oracle only
+if the ghost protocol delivered every needed point.
+"""
+import numpy as np
+import torch
+
+from oracle import knn_brute
+from oracle import tree as T
+
+
+class CpuIndex:
+    def __init__(self, pts4, n_query, box):
+        self.pts4 = pts4.cpu().numpy()
+        self.n = self.pts4.shape[0]
+        self.n_query = n_query
+        self.box = box
+        self.device = torch.device("cpu")
+
+
+class CpuBackend:
+    def morton_keys(self, pos, frame):
+        p = pos.numpy()
+        if frame["box"] is not None:
+            o, s = T.key_frame(p, frame["box"])
+        else:
+            o = np.asarray(frame["origin"], np.float32)
+            s = np.full(3, np.float32(2.0 ** T.BITS / frame["extent"]), np.float32)
+        return torch.from_numpy(T.morton_keys(T.quantize(p, o, s, is_scale=True)).astype(np.int64))
+
+    def bbox(self, pos):
+        return pos.min(0).values.clone(), pos.max(0).values.clone()
+
+    def sample(self, keys, n, seed):
+        if keys.shape[0] == 0:
+            return keys[:0]
+        rng = np.random.default_rng(seed)
+        return keys[torch.from_numpy(rng.integers(0, keys.shape[0], n))]
+
+    def sort_samples(self, s):
+        return torch.sort(s).values
+
+    def bucket(self, keys, spl):
+        dest = np.searchsorted(spl.numpy(), keys.numpy(), side="right").astype(np.int32)
+        counts = np.bincount(dest, minlength=spl.shape[0] + 1)
+        return torch.from_numpy(dest), [int(c) for c in counts]
+
+    def pack(self, pos, gbase, dest, counts):
+        d = dest.numpy()
+        order = np.argsort(d, kind="stable")
+        p = pos.numpy()[order]
+        g = (gbase + order).astype(np.int32).view(np.float32)
+        return torch.from_numpy(np.concatenate([p, g[:, None]], axis=1).astype(np.float32))
+
+    def build(self, pts4, n_query, box):
+        return CpuIndex(pts4, n_query, box)
+
+    def query_boxes(self, ix, k, rank):
+        """Chunks of 64 local points (key order): AABB + max local k-th d2 (a valid bound:
+        the local k-th distance can only shrink when more points are added)."""
+        p = ix.pts4[:, :3]
+        n = p.shape[0]
+        if n < k:
+            r2 = np.full(n, np.inf)
+        else:
+            _, d2 = knn_brute(p, k, ix.box)
+            r2 = d2[:, -1].astype(np.float64)
+        o, s = T.key_frame(p, ix.box) if ix.box is not None else T.key_frame(p)
+        order = np.argsort(T.morton_keys(T.quantize(p, o, s, is_scale=True)), kind="stable")
+        rows = []
+        for c in range(0, n, 64):
+            sel = order[c:c + 64]
+            lo, hi = p[sel].min(0), p[sel].max(0)
+            rows.append([*lo, r2[sel].max(), *hi, np.float32(rank).view(np.int32).view(np.float32)])
+        out = np.asarray(rows, np.float32)
+        out[:, 7] = np.array([rank] * len(rows), np.int32).view(np.float32)
+        return torch.from_numpy(out)
+
+    def select_ghosts(self, ix, boxes, rank, R):
+        b = boxes.numpy()
+        p = ix.pts4[:, :3].astype(np.float64)
+        mask = np.zeros(ix.n, np.int32)
+        rk = b[:, 7].view(np.int32)
+        for j in range(b.shape[0]):
+            if rk[j] == rank:
+                continue
+            lo, hi = b[j, 0:3].astype(np.float64), b[j, 4:7].astype(np.float64)
+            gap = np.maximum(0.0, np.maximum(lo - p, p - hi))
+            if ix.box is not None:  # minimal image of the point-box gap
+                L = np.broadcast_to(np.asarray(ix.box, np.float64), (3,))
+                c = 0.5 * (lo + hi)
+                e = 0.5 * (hi - lo)
+                dd = np.abs(p - c)
+                dd = np.minimum(dd, L - dd)
+                gap = np.maximum(0.0, dd - e)
+            d = np.sqrt((gap ** 2).sum(1))
+            r = np.sqrt(np.float64(b[j, 3]))
+            hit = d <= r * (1 + 1e-5) + 1e-7
+            mask[hit] |= 1 << int(rk[j])
+        counts = [int(((mask >> r) & 1).sum()) for r in range(R)]
+        return torch.from_numpy(mask), counts
+
+    def pack_ghosts(self, ix, mask, counts):
+        m = mask.numpy()
+        parts = [ix.pts4[((m >> r) & 1) == 1] for r in range(len(counts))]
+        return torch.from_numpy(np.concatenate(parts).astype(np.float32)) if parts else torch.zeros((0, 4))
+
+    def query_z(self, ix, k):
+        p = ix.pts4[:, :3]
+        g = ix.pts4[:, 3].view(np.int32)
+        rows = np.arange(ix.n_query)
+        idx, d2 = knn_brute(p, k, ix.box, rows=rows)
+        return torch.from_numpy(g[idx]), torch.from_numpy(d2), torch.from_numpy(g[:ix.n_query].copy())
+
+    def free(self, ix):
+        pass

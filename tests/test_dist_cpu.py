@@ -1,0 +1,76 @@
+"""World-size-2/3 gloo tests (CPU) of the multi-GPU orchestration in
+paper_2604_05885_b200.dist: sample splitters, Morton-range redistribution, query boxes and the
+ghost exchange, z-order rows with global ids. The per-rank stages are the CPU stand-ins of
+tests/cpu_backend.py; the gathered result must equal the oracle on the whole set (rank
+transparency)."""
+import os
+import socket
+import tempfile
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+from oracle import knn_brute
+from synth import clustered_points, uniform_points
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, n, kind, box, k, out_dir):
+    import torch.distributed as dist
+
+    from paper_2604_05885_b200.dist import TorchComm, dist_knn
+    from tests.cpu_backend import CpuBackend
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    gen = uniform_points if kind == "uniform" else clustered_points
+    lo, hi = (n * rank) // world, (n * (rank + 1)) // world
+    pos = torch.from_numpy(gen(n, 7, 1.0, start=lo, stop=hi))
+    if kind == "octant":  # adversarial: everything in one corner, ranks hold each other's neighbours
+        pos = pos * 0.125
+    idx, d2, rowg = dist_knn(pos, lo, k, box, TorchComm(), CpuBackend(), n_samp=64, seed=3)
+    np.savez(os.path.join(out_dir, f"r{rank}.npz"), idx=idx.numpy(), d2=d2.numpy(), rowg=rowg.numpy())
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("kind,box", [("uniform", 1.0), ("clustered", 1.0), ("clustered", None), ("octant", None)])
+def test_gloo_dist_knn_equals_oracle(world, kind, box):
+    n, k = 1500, 8
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_worker, args=(world, _free_port(), n, kind, box, k, d), nprocs=world, join=True)
+        idx = np.full((n, k), -1, np.int32)
+        d2 = np.zeros((n, k), np.float32)
+        owned = []
+        for r in range(world):
+            z = np.load(os.path.join(d, f"r{r}.npz"))
+            idx[z["rowg"]] = z["idx"]
+            d2[z["rowg"]] = z["d2"]
+            owned.append(len(z["rowg"]))
+    assert sum(owned) == n and min(owned) > 0
+    gen = uniform_points if kind == "uniform" else clustered_points
+    pos = gen(n, 7, 1.0)
+    if kind == "octant":
+        pos = (pos * 0.125).astype(np.float32)
+    io, do = knn_brute(pos, k, box)
+    assert np.array_equal(idx, io)
+    assert np.array_equal(d2.view(np.int32), do.view(np.int32))
+
+
+def test_splitters_quantiles():
+    from paper_2604_05885_b200.dist import splitters_from_samples
+
+    s = torch.arange(100, dtype=torch.int64).flip(0)
+    spl = splitters_from_samples(s, 4, lambda x: torch.sort(x).values)
+    assert spl.tolist() == [25, 50, 75]
+    assert splitters_from_samples(s, 1, lambda x: torch.sort(x).values).numel() == 0
