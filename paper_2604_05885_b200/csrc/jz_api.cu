@@ -75,7 +75,7 @@ jz_knn_params normalize(const jz_knn_params *p) {
   jz_knn_params r;
   memset(&r, 0, sizeof(r));
   if (p) r = *p;
-  if (r.nmax0 <= 0) r.nmax0 = 48;
+  if (r.nmax0 <= 0) r.nmax0 = 128;  // larger leaves amortise the walk (paper default 48)
   if (r.coarsen <= 0) r.coarsen = 8;
   if (r.ntarget <= 0) r.ntarget = 1000;
   if (r.ngr <= 0) r.ngr = 32;

@@ -5,7 +5,7 @@
 // Layout: an interaction list at plane level p is (ispl [nrecv+1] int64, isrc int32, rlow f32)
 // with rlow = d_low^2 of the (receiver, source) pair. Receivers at level p+1 are "parents";
 // the kernels below move the list one plane down:
-//   k_n2n<RMAX>   one CTA per receiving parent, one thread per child: a register
+//   k_n2n<RMAX>   one warp per receiving parent, one lane per child: a register
 //                 count-heap of N_r = 8 (d_up^2, count) entries over the children of
 //                 every source parent in the segment, staged in shared memory -> R_max^2.
 //   k_n2n<COUNT>  #source children with d_low^2 <= R_max^2
@@ -21,8 +21,6 @@
 
 namespace jz {
 
-constexpr int kN2NThreads = 64;
-constexpr int kN2NStage = 256;  // source children staged per round (8 KB)
 constexpr int kHeap = 8;        // N_r (R13)
 
 enum { RMAX = 0, COUNT = 1, INSERT = 2 };
@@ -111,20 +109,29 @@ __device__ __forceinline__ void heap_insert(CountHeap &h, float r, int c, int k)
   }
 }
 
+// One warp per receiving parent (4 parents per CTA), one lane per child; the source
+// parent's children are staged in the warp's shared-memory slot. Warps are independent
+// (no CTA barriers); the RMAX early exit is a warp vote.
+constexpr int kN2NWarps = 4;
+constexpr int kN2NWStage = 128;  // staged source children per warp (4 KB)
+
 template <int MODE>
-__global__ void __launch_bounds__(kN2NThreads) k_n2n(const int32_t *__restrict__ pbeg, const int64_t *__restrict__ ispl,
-                                                     const int32_t *__restrict__ isrc, const float *__restrict__ rlow,
-                                                     const NodeBox *__restrict__ cbox, Dom D, int k, int sorted,
-                                                     int early, float *__restrict__ rmax2, int32_t *__restrict__ cnt,
-                                                     const int64_t *__restrict__ ispl_out,
-                                                     int32_t *__restrict__ isrc_out, float *__restrict__ rlow_out) {
-  __shared__ NodeBox s_box[kN2NStage];
-  __shared__ float s_red[kN2NThreads / 32];
-  const int J = blockIdx.x;
+__global__ void __launch_bounds__(kN2NWarps * 32) k_n2n(const int32_t *__restrict__ pbeg, int64_t npar,
+                                                       const int64_t *__restrict__ ispl,
+                                                       const int32_t *__restrict__ isrc, const float *__restrict__ rlow,
+                                                       const NodeBox *__restrict__ cbox, Dom D, int k, int sorted,
+                                                       int early, float *__restrict__ rmax2, int32_t *__restrict__ cnt,
+                                                       const int64_t *__restrict__ ispl_out,
+                                                       int32_t *__restrict__ isrc_out, float *__restrict__ rlow_out) {
+  __shared__ NodeBox s_box[kN2NWarps][kN2NWStage];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t J = (int64_t)blockIdx.x * kN2NWarps + warp;
+  if (J >= npar) return;
+  NodeBox *sb = s_box[warp];
   const int cb = pbeg[J], ce = pbeg[J + 1];
   const int64_t eb = ispl[J], ee = ispl[J + 1];
-  for (int c0 = cb; c0 < ce; c0 += kN2NThreads) {
-    const int i = c0 + threadIdx.x;
+  for (int c0 = cb; c0 < ce; c0 += 32) {
+    const int i = c0 + lane;
     const bool valid = i < ce;
     NodeBox mb;
     if (valid) mb = cbox[i];
@@ -143,37 +150,30 @@ __global__ void __launch_bounds__(kN2NThreads) k_n2n(const int32_t *__restrict__
     } else {
       R = valid ? rmax2[i] : 0.f;
       if (MODE == INSERT && valid) wp = ispl_out[i];
-      float m = R;
+      Rchunk = R;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-      if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = m;
-      __syncthreads();
-      Rchunk = s_red[0];
-#pragma unroll
-      for (int w = 1; w < kN2NThreads / 32; ++w) Rchunk = fmaxf(Rchunk, s_red[w]);
+      for (int o = 16; o > 0; o >>= 1) Rchunk = fmaxf(Rchunk, __shfl_xor_sync(0xffffffffu, Rchunk, o));
     }
     for (int64_t e = eb; e < ee; ++e) {
       const int S = isrc[e];
       const float rl = rlow[e];
       if (early) {
         // early exit: no child can use this entry (d_low of children >= rl)
-        bool need;
-        if (MODE == RMAX) need = __syncthreads_or(valid && rl < R);
-        else need = rl <= Rchunk;
+        const bool need = MODE == RMAX ? __any_sync(0xffffffffu, valid && rl < R) : rl <= Rchunk;
         if (!need) {
           if (sorted) break;
           continue;
         }
       }
-      const int sb = pbeg[S], se = pbeg[S + 1];
-      for (int s0 = sb; s0 < se; s0 += kN2NStage) {
-        const int sn = min(kN2NStage, se - s0);
-        __syncthreads();
-        for (int t = threadIdx.x; t < sn; t += kN2NThreads) s_box[t] = cbox[s0 + t];
-        __syncthreads();
+      const int sb0 = pbeg[S], se = pbeg[S + 1];
+      for (int s0 = sb0; s0 < se; s0 += kN2NWStage) {
+        const int sn = min(kN2NWStage, se - s0);
+        __syncwarp();
+        for (int t = lane; t < sn; t += 32) sb[t] = cbox[s0 + t];
+        __syncwarp();
         if (valid) {
           for (int t = 0; t < sn; ++t) {
-            const NodeBox sbx = s_box[t];
+            const NodeBox sbx = sb[t];
             if (MODE == RMAX) {
               const float r2 = box_dup2(mb, sbx, D);
               if (r2 < R) {
@@ -199,7 +199,6 @@ __global__ void __launch_bounds__(kN2NThreads) k_n2n(const int32_t *__restrict__
       if (MODE == RMAX) rmax2[i] = R;
       if (MODE == COUNT) cnt[i] = count;
     }
-    __syncthreads();
   }
 }
 
@@ -281,10 +280,10 @@ void walk_to(const std::vector<Plane> &planes, const Dom &D, int k, int ngr, uns
     JZ_CUDA(cudaMallocAsync(&cnt, pl.nnodes * sizeof(int32_t), st));
     const int srt = do_sort ? 1 : 0;
     const int ee = early ? 1 : 0;
-    k_n2n<RMAX><<<(unsigned)npar, kN2NThreads, 0, st>>>(pbeg, il.ispl, il.isrc, il.rlow, pl.box, D, k, srt, ee,
+    k_n2n<RMAX><<<(unsigned)ceil_div(npar, kN2NWarps), kN2NWarps * 32, 0, st>>>(pbeg, npar, il.ispl, il.isrc, il.rlow, pl.box, D, k, srt, ee,
                                                         rmax2, nullptr, nullptr, nullptr, nullptr);
     JZ_LAUNCH_CHECK();
-    k_n2n<COUNT><<<(unsigned)npar, kN2NThreads, 0, st>>>(pbeg, il.ispl, il.isrc, il.rlow, pl.box, D, k, srt, ee,
+    k_n2n<COUNT><<<(unsigned)ceil_div(npar, kN2NWarps), kN2NWarps * 32, 0, st>>>(pbeg, npar, il.ispl, il.isrc, il.rlow, pl.box, D, k, srt, ee,
                                                          rmax2, cnt, nullptr, nullptr, nullptr);
     JZ_LAUNCH_CHECK();
     IList nl;
@@ -294,7 +293,7 @@ void walk_to(const std::vector<Plane> &planes, const Dom &D, int k, int ngr, uns
     nl.total = read_i64(nl.ispl + pl.nnodes, st);
     JZ_CUDA(cudaMallocAsync(&nl.isrc, (nl.total > 0 ? nl.total : 1) * sizeof(int32_t), st));
     JZ_CUDA(cudaMallocAsync(&nl.rlow, (nl.total > 0 ? nl.total : 1) * sizeof(float), st));
-    k_n2n<INSERT><<<(unsigned)npar, kN2NThreads, 0, st>>>(pbeg, il.ispl, il.isrc, il.rlow, pl.box, D, k, srt, ee,
+    k_n2n<INSERT><<<(unsigned)ceil_div(npar, kN2NWarps), kN2NWarps * 32, 0, st>>>(pbeg, npar, il.ispl, il.isrc, il.rlow, pl.box, D, k, srt, ee,
                                                           rmax2, nullptr, nl.ispl, nl.isrc, nl.rlow);
     JZ_LAUNCH_CHECK();
     if (do_sort) {
