@@ -59,7 +59,8 @@ enum { JZ_ORDER_INPUT = 0, JZ_ORDER_Z = 1 };
 enum {
   JZ_FLAG_FRAME = 1u << 0,         /* use frame_origin / frame_extent for the Morton keys (multi-GPU: one global frame) */
   JZ_FLAG_NO_EARLY_EXIT = 1u << 1, /* disable the sorted-r_low early exit (pruning-safety tests) */
-  JZ_FLAG_NO_SEGSORT = 1u << 2     /* do not sort interaction segments by r_low (implies no early exit) */
+  JZ_FLAG_NO_SEGSORT = 1u << 2,    /* do not sort interaction segments by r_low (implies no early exit) */
+  JZ_FLAG_WS_LEAF = 1u << 13       /* experimental: warp-specialised LeafToLeaf (producer warp + mbarrier ring) */
 };
 
 /* Tree / walk parameters. Zero fields take the defaults (nmax0 see DESIGN.md §6). */

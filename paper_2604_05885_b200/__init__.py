@@ -20,7 +20,7 @@ import numpy as np
 import torch
 
 from . import _binding as B
-from ._binding import JzError, JZ_FLAG_FRAME, JZ_FLAG_NO_EARLY_EXIT, JZ_FLAG_NO_SEGSORT  # noqa: F401
+from ._binding import JzError, JZ_FLAG_FRAME, JZ_FLAG_NO_EARLY_EXIT, JZ_FLAG_NO_SEGSORT, JZ_FLAG_WS_LEAF  # noqa: F401
 
 __all__ = ["KnnIndex", "knn", "knn_host", "JzError", "set_timing"]
 

@@ -103,6 +103,7 @@ struct LeafPK {
   float *out_d2;
   int32_t *out_row_gidx;
   unsigned long long *stats;  // [0] distance evaluations, [1] top-k insertions (or nullptr)
+  const float *seed_d2;       // diagnostics only: per-row k-th d2 of a previous run (or nullptr)
 };
 
 // per-axis shift class of a (query box, source box) pair: 0 = no wrap for any pair,
@@ -347,7 +348,11 @@ __global__ void __launch_bounds__(kLThreads) k_leaf(LeafPK a, Dom D) {
   wbox.lo = make_float4(blo[0], blo[1], blo[2], 0.f);
   wbox.hi = make_float4(bhi[0], bhi[1], bhi[2], 0.f);
 
-  const float R0 = a.rmax2 ? a.rmax2[J] : INFINITY;
+  float R0 = a.rmax2 ? a.rmax2[J] : INFINITY;
+  if (a.seed_d2 && act) {
+    const int64_t row = a.order == JZ_ORDER_INPUT ? (int64_t)inpos : (a.zrow ? (int64_t)a.zrow[qi] : (int64_t)qi);
+    R0 = a.seed_d2[row * a.k + a.k - 1];
+  }
   Lane<K> L;
   {
     const u64 sentinel = ((u64)__float_as_uint(R0) << 32) | 0xffffffffull;
@@ -413,25 +418,460 @@ __global__ void __launch_bounds__(kLThreads) k_leaf(LeafPK a, Dom D) {
   }
 }
 
+// =====================================================================================
+// Warp-specialised LeafToLeaf (experimental, JZ_FLAG_WS_LEAF; slower than k_leaf in round 1:
+// the single producer warp's dependent-load chain starves the consumers). One CTA per work item = up to 128 consecutive queries
+// of a receiving plane-1 node J: warp 0 is the producer, warps 1..4 are consumers (32 queries
+// each). The producer walks J's interaction list once for all 128 queries (J's own leaves
+// first, then the list in r_low order), prunes leaves with the exact box bound against the
+// CTA's query box and the consumers' published k-th bounds, and stages surviving leaves as
+// NaN-padded x/y/z/gidx arrays into a 3-slot shared-memory ring. Full/empty mbarriers hand
+// slots over: consumers never stall on the walk's dependent loads, and the walk and staging
+// are shared by four warps. Each consumer re-tests every staged leaf against its own query box
+// and lanes, evaluates survivors with the packed f32x2 loop and drains its candidate queue
+// once per slot.
+// =====================================================================================
+constexpr int kWC = 4;                 // consumer warps
+constexpr int kWThreads = (kWC + 1) * 32;
+constexpr int kRS = 3;                 // ring slots
+constexpr int kSCap = 256;             // staged points per slot
+constexpr int kSSeg = 32;              // leaves per slot
+
+struct Slot {
+  float x[kSCap], y[kSCap], z[kSCap];
+  int g[kSCap];
+  NodeBox box[kSSeg];
+  int off[kSSeg], len[kSSeg], leaf[kSSeg];
+  int nseg;  // -1 = end of stream
+};
+
+struct WSShared {
+  Slot ring[kRS];
+  Slot own[kWC];  // consumers' private slot for their own-leaf pre-pass
+  u64 q[kWC][kQCap][32];
+  unsigned long long full[kRS], empty[kRS];
+  float wmax[kWC];
+  NodeBox wbox[kWC];
+};
+
+__device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long *bar) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+
+template <int K>
+__device__ __forceinline__ void wflush(u64 (*q)[32], Lane<K> &L) {
+  const int lane = threadIdx.x & 31;
+  const int mx = __reduce_max_sync(0xffffffffu, (unsigned)L.qn);
+  for (int i = 0; i < mx; ++i) {
+    if (i < L.qn) {
+      const u64 key = q[i][lane];
+      if (key < L.tk[K - 1]) {
+        topk_insert<K>(L.tk, key);
+        ++L.ins;
+      }
+    }
+  }
+  L.kth = L.act ? __uint_as_float((unsigned)(L.tk[K - 1] >> 32)) : -1.f;
+  L.qn = 0;
+}
+
+template <int K>
+__device__ __forceinline__ void wenqueue(u64 (*q)[32], Lane<K> &L, float d2, int g) {
+  if (d2 <= L.kth) {
+    q[L.qn][threadIdx.x & 31] = ((u64)__float_as_uint(d2) << 32) | (unsigned)(g + 1);
+    ++L.qn;
+  }
+}
+
+// staged sources [j0, j0 + n) of a slot (n multiple of 4, NaN padded) against the lane's query
+template <int K, bool SHIFT>
+__device__ __forceinline__ void weval(const Slot &S, u64 (*q)[32], int j0, int n, float qx, float qy, float qz,
+                                      float shx, float shy, float shz, Lane<K> &L) {
+  const u64 QX = pk(qx, qx), QY = pk(qy, qy), QZ = pk(qz, qz);
+  const u64 SX = pk(shx, shx), SY = pk(shy, shy), SZ = pk(shz, shz);
+  for (int j = j0; j < j0 + n; j += 4) {
+    const float4 X = *reinterpret_cast<const float4 *>(&S.x[j]);
+    const float4 Y = *reinterpret_cast<const float4 *>(&S.y[j]);
+    const float4 Z = *reinterpret_cast<const float4 *>(&S.z[j]);
+    u64 tx0 = sub2(QX, pk(X.x, X.y)), tx1 = sub2(QX, pk(X.z, X.w));
+    u64 ty0 = sub2(QY, pk(Y.x, Y.y)), ty1 = sub2(QY, pk(Y.z, Y.w));
+    u64 tz0 = sub2(QZ, pk(Z.x, Z.y)), tz1 = sub2(QZ, pk(Z.z, Z.w));
+    if (SHIFT) {
+      tx0 = add2(tx0, SX);
+      tx1 = add2(tx1, SX);
+      ty0 = add2(ty0, SY);
+      ty1 = add2(ty1, SY);
+      tz0 = add2(tz0, SZ);
+      tz1 = add2(tz1, SZ);
+    }
+    const u64 d0 = fma2(tz0, tz0, fma2(ty0, ty0, mul2(tx0, tx0)));
+    const u64 d1 = fma2(tz1, tz1, fma2(ty1, ty1, mul2(tx1, tx1)));
+    float a0, a1, a2, a3;
+    upk(d0, a0, a1);
+    upk(d1, a2, a3);
+    const float m = fminf(fminf(a0, a1), fminf(a2, a3));
+    if (__any_sync(0xffffffffu, m <= L.kth)) {
+      if (__any_sync(0xffffffffu, L.qn > kQCap - 4)) wflush<K>(q, L);  // room for 4
+      const int4 G = *reinterpret_cast<const int4 *>(&S.g[j]);
+      wenqueue<K>(q, L, a0, G.x);
+      wenqueue<K>(q, L, a1, G.y);
+      wenqueue<K>(q, L, a2, G.z);
+      wenqueue<K>(q, L, a3, G.w);
+    }
+  }
+}
+
+template <int K>
+__device__ __forceinline__ void weval_generic(const Slot &S, u64 (*q)[32], int j0, int n, float qx, float qy,
+                                              float qz, const Dom &D, Lane<K> &L) {
+  for (int j = j0; j < j0 + n; ++j) {
+    const float d2 = canon_d2_per(qx, qy, qz, S.x[j], S.y[j], S.z[j], D);  // NaN padding -> NaN
+    if (__any_sync(0xffffffffu, L.qn >= kQCap)) wflush<K>(q, L);       // room for 1
+    wenqueue<K>(q, L, d2, S.g[j]);
+  }
+}
+
+template <int K, bool PER>
+__device__ __forceinline__ void wslot(const LeafPK &a, const Dom &D, const Slot &S, int ns, int xa, int xb,
+                                      const NodeBox &wbox, float qx, float qy, float qz, bool act, u64 (*q)[32],
+                                      Lane<K> &L, unsigned long long &nev) {
+  for (int s = 0; s < ns; ++s) {
+    const int lf = S.leaf[s];
+    if (lf >= xa && lf < xb) continue;  // evaluated in the pre-pass
+    const NodeBox bx = S.box[s];
+    const float wm = a.early ? warp_max_kth(L.kth) : INFINITY;
+    if (box_dlow2(wbox, bx, D) > wm) continue;
+    if (!__any_sync(0xffffffffu, act && pt_box_dlow2(qx, qy, qz, bx, D) <= L.kth)) continue;
+    const int off = S.off[s], m = S.len[s], mp = (m + 3) & ~3;
+    nev += act ? (unsigned)m : 0u;
+    int cls = 0;
+    float s0 = 0.f, s1 = 0.f, s2 = 0.f;
+    if (PER) {
+      cls = shift_class(wbox.lo.x, wbox.hi.x, bx.lo.x, bx.hi.x, D.L[0], D.h[0], s0);
+      cls |= shift_class(wbox.lo.y, wbox.hi.y, bx.lo.y, bx.hi.y, D.L[1], D.h[1], s1) << 2;
+      cls |= shift_class(wbox.lo.z, wbox.hi.z, bx.lo.z, bx.hi.z, D.L[2], D.h[2], s2) << 4;
+    }
+    if (!PER || cls == 0) weval<K, false>(S, q, off, mp, qx, qy, qz, 0.f, 0.f, 0.f, L);
+    else if (!any_straddle(cls)) weval<K, true>(S, q, off, mp, qx, qy, qz, s0, s1, s2, L);
+    else weval_generic<K>(S, q, off, mp, qx, qy, qz, D, L);
+  }
+  if (__any_sync(0xffffffffu, L.qn > 0)) wflush<K>(q, L);
+}
+
+struct ItemWS {
+  const int32_t *item_par;
+  const int32_t *item_q0;
+  int64_t nitems;
+};
+
+template <int K, bool PER>
+__global__ void __launch_bounds__(kWThreads) k_leafws(LeafPK a, ItemWS it, Dom D) {
+  extern __shared__ __align__(16) unsigned char s_raw[];
+  WSShared &W = *reinterpret_cast<WSShared *>(s_raw);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t item = blockIdx.x;
+  const int J = it.item_par[item];
+  const int LJa = a.par_leaf[J], LJb = a.par_leaf[J + 1];
+  const int qhi = a.leaf_beg[LJb];
+  const int q0 = it.item_q0[item];
+  const float R0 = a.rmax2 ? a.rmax2[J] : INFINITY;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kRS; ++s) {
+      mbar_init(&W.full[s], 1);
+      mbar_init(&W.empty[s], kWC);
+    }
+  }
+  // ---- consumer setup
+  const int cw = warp - 1;
+  const int qi = q0 + cw * 32 + lane;
+  bool act = false;
+  float qx = 0.f, qy = 0.f, qz = 0.f, qw = 0.f;
+  int inpos = 0;
+  Lane<K> L;
+  NodeBox wbox;
+  bool wact = false;
+  if (warp > 0) {
+    act = qi < qhi && cw * 32 < 128;
+    if (act) {
+      const float4 qq = a.pts[qi];
+      qx = qq.x;
+      qy = qq.y;
+      qz = qq.z;
+      qw = qq.w;
+      inpos = a.perm[qi];
+      act = inpos < a.n_query;
+    }
+    wact = __any_sync(0xffffffffu, act);
+    float blo[3] = {act ? qx : INFINITY, act ? qy : INFINITY, act ? qz : INFINITY};
+    float bhi[3] = {act ? qx : -INFINITY, act ? qy : -INFINITY, act ? qz : -INFINITY};
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        blo[d] = fminf(blo[d], __shfl_xor_sync(0xffffffffu, blo[d], o));
+        bhi[d] = fmaxf(bhi[d], __shfl_xor_sync(0xffffffffu, bhi[d], o));
+      }
+    }
+    wbox.lo = make_float4(blo[0], blo[1], blo[2], 0.f);
+    wbox.hi = make_float4(bhi[0], bhi[1], bhi[2], 0.f);
+    const u64 sentinel = ((u64)__float_as_uint(R0) << 32) | 0xffffffffull;
+#pragma unroll
+    for (int j = 0; j < K; ++j) L.tk[j] = (j < K - a.k) ? 0ull : sentinel;
+    L.kth = act ? R0 : -1.f;
+    L.ins = 0;
+    L.qn = 0;
+    L.act = act;
+    if (lane == 0) {
+      W.wbox[cw] = wbox;
+      W.wmax[cw] = wact ? R0 : -1.f;
+    }
+  }
+  __syncthreads();
+
+  if (warp == 0) {
+    // ================= producer =================
+    NodeBox cb;
+    cb.lo = make_float4(INFINITY, INFINITY, INFINITY, 0.f);
+    cb.hi = make_float4(-INFINITY, -INFINITY, -INFINITY, 0.f);
+#pragma unroll
+    for (int w = 0; w < kWC; ++w) {
+      if (W.wmax[w] >= 0.f) {
+        cb.lo.x = fminf(cb.lo.x, W.wbox[w].lo.x);
+        cb.lo.y = fminf(cb.lo.y, W.wbox[w].lo.y);
+        cb.lo.z = fminf(cb.lo.z, W.wbox[w].lo.z);
+        cb.hi.x = fmaxf(cb.hi.x, W.wbox[w].hi.x);
+        cb.hi.y = fmaxf(cb.hi.y, W.wbox[w].hi.y);
+        cb.hi.z = fmaxf(cb.hi.z, W.wbox[w].hi.z);
+      }
+    }
+    int itn = 0, n = 0, ns = 0;
+    Slot *S = &W.ring[0];
+    mbar_wait(&W.empty[0], 1);
+    auto bound = [&]() {
+      if (!a.early) return INFINITY;
+      float m = -1.f;
+#pragma unroll
+      for (int w = 0; w < kWC; ++w) m = fmaxf(m, ((volatile float *)W.wmax)[w]);
+      return m;
+    };
+    auto commit = [&](int nseg) {
+      __syncwarp();
+      if (lane == 0) {
+        S->nseg = nseg;
+        mbar_arrive(&W.full[itn % kRS]);
+      }
+      ++itn;
+      S = &W.ring[itn % kRS];
+      mbar_wait(&W.empty[itn % kRS], ((itn / kRS) & 1) ^ 1);
+      n = 0;
+      ns = 0;
+    };
+    const int64_t eb = a.ispl[J], ee = a.ispl[J + 1];
+    // own node J first (its leaves hold the queries), then the list in r_low order
+    for (int64_t e = eb - 1; e < ee; ++e) {
+      int Sx = J;
+      float wm = bound();
+      if (e >= eb) {
+        Sx = a.isrc[e];
+        if (Sx == J) continue;
+        if (a.rlow[e] > wm) {
+          if (a.sorted) break;
+          continue;
+        }
+        if (a.par_box && box_dlow2(cb, a.par_box[Sx], D) > wm) continue;
+      }
+      const int la = a.par_leaf[Sx], lb = a.par_leaf[Sx + 1];
+      for (int l0 = la; l0 < lb; l0 += 32) {
+        // lane-parallel: box test, leaf range and box of one leaf per lane (independent loads)
+        const int l = l0 + lane;
+        bool pass = false;
+        NodeBox lbx;
+        int lp0 = 0, lp1 = 0;
+        if (l < lb) {
+          lbx = a.leaf_box[l];
+          lp0 = a.leaf_beg[l];
+          lp1 = a.leaf_beg[l + 1];
+          pass = e < eb || box_dlow2(cb, lbx, D) <= wm;
+        }
+        unsigned bal = __ballot_sync(0xffffffffu, pass);
+        while (bal) {
+          const int src = __ffs(bal) - 1;
+          bal &= bal - 1;
+          const int lf = l0 + src;
+          const int lp = __shfl_sync(0xffffffffu, lp0, src);
+          const int m = __shfl_sync(0xffffffffu, lp1, src) - lp, mp = (m + 3) & ~3;
+          if (n + mp > kSCap || ns == kSSeg) commit(ns);
+          // all loads of the leaf first (up to 4 per lane), then the stores
+          float4 pv[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int t = lane + 32 * u;
+            pv[u] = make_float4(__int_as_float(0x7fc00000), __int_as_float(0x7fc00000), __int_as_float(0x7fc00000),
+                                0.f);
+            if (t < m) pv[u] = a.pts[lp + t];
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int t = lane + 32 * u;
+            if (t < mp) {
+              S->x[n + t] = pv[u].x;
+              S->y[n + t] = pv[u].y;
+              S->z[n + t] = pv[u].z;
+              S->g[n + t] = __float_as_int(pv[u].w);
+            }
+          }
+          if (lane == src) {
+            S->box[ns] = lbx;
+            S->off[ns] = n;
+            S->len[ns] = m;
+            S->leaf[ns] = lf;
+          }
+          n += mp;
+          ++ns;
+        }
+      }
+    }
+    if (ns > 0) commit(ns);
+    __syncwarp();
+    if (lane == 0) {
+      S->nseg = -1;
+      mbar_arrive(&W.full[itn % kRS]);
+    }
+    return;
+  }
+
+  // ================= consumers =================
+  u64(*q)[32] = W.q[cw];
+  unsigned long long nev = 0;
+  // pre-pass: this warp's own leaves (the leaves holding its 32 queries), staged privately
+  int xa = 0x7fffffff, xb = -1;
+  if (wact) {
+    const int qb = q0 + cw * 32, qend = min(qb + 32, qhi);
+    for (int l0 = LJa; l0 < LJb; l0 += 32) {
+      const int l = l0 + lane;
+      const bool ov = l < LJb && a.leaf_beg[l] < qend && a.leaf_beg[l + 1] > qb;
+      const unsigned b = __ballot_sync(0xffffffffu, ov);
+      if (b) {
+        xa = min(xa, l0 + __ffs(b) - 1);
+        xb = max(xb, l0 + 32 - __clz(b));
+      }
+    }
+    Slot &O = W.own[cw];
+    int n = 0, ns = 0;
+    for (int lf = xa; lf < xb; ++lf) {
+      const int lp = a.leaf_beg[lf], m = a.leaf_beg[lf + 1] - lp, mp = (m + 3) & ~3;
+      if (n + mp > kSCap || ns == kSSeg) {
+        __syncwarp();
+        wslot<K, PER>(a, D, O, ns, -1, -1, wbox, qx, qy, qz, act, q, L, nev);
+        __syncwarp();
+        n = ns = 0;
+      }
+      for (int t = lane; t < mp; t += 32) {
+        float4 p = make_float4(__int_as_float(0x7fc00000), __int_as_float(0x7fc00000), __int_as_float(0x7fc00000), 0.f);
+        if (t < m) p = a.pts[lp + t];
+        O.x[n + t] = p.x;
+        O.y[n + t] = p.y;
+        O.z[n + t] = p.z;
+        O.g[n + t] = __float_as_int(p.w);
+      }
+      if (lane == 0) {
+        O.box[ns] = a.leaf_box[lf];
+        O.off[ns] = n;
+        O.len[ns] = m;
+        O.leaf[ns] = lf;
+      }
+      n += mp;
+      ++ns;
+    }
+    __syncwarp();
+    if (ns) wslot<K, PER>(a, D, O, ns, -1, -1, wbox, qx, qy, qz, act, q, L, nev);
+    const float wmk = warp_max_kth(L.kth);
+    if (lane == 0) W.wmax[cw] = wmk;
+  }
+  for (int itn = 0;; ++itn) {
+    const int sl = itn % kRS;
+    mbar_wait(&W.full[sl], (itn / kRS) & 1);
+    const Slot &S = W.ring[sl];
+    const int ns = S.nseg;
+    if (ns < 0) break;
+    if (wact) {
+      wslot<K, PER>(a, D, S, ns, xa, xb, wbox, qx, qy, qz, act, q, L, nev);
+      const float wmk = warp_max_kth(L.kth);  // all lanes (warp reduction)
+      if (lane == 0) W.wmax[cw] = wmk;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&W.empty[sl]);
+  }
+  if (a.stats) {
+    unsigned long long tot = nev, ins = L.ins;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      tot += __shfl_xor_sync(0xffffffffu, tot, o);
+      ins += __shfl_xor_sync(0xffffffffu, ins, o);
+    }
+    if (lane == 0) {
+      atomicAdd(&a.stats[0], tot);
+      atomicAdd(&a.stats[1], ins);
+    }
+  }
+  if (act) {
+    const int64_t row = a.order == JZ_ORDER_INPUT ? (int64_t)inpos : (a.zrow ? (int64_t)a.zrow[qi] : (int64_t)qi);
+    int32_t *oi = a.out_idx + row * a.k;
+    float *od = a.out_d2 + row * a.k;
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      if (j >= K - a.k) {
+        oi[j - (K - a.k)] = (int32_t)((unsigned)(L.tk[j] & 0xffffffffu) - 1u);
+        od[j - (K - a.k)] = __uint_as_float((unsigned)(L.tk[j] >> 32));
+      }
+    }
+    if (a.out_row_gidx) a.out_row_gidx[row] = __float_as_int(qw);
+  }
+}
+
 // work items: 32-query groups of each receiving parent, in z order
 __global__ void k_item_count(const int32_t *__restrict__ par_leaf, const int32_t *__restrict__ leaf_beg, int64_t npar,
-                             int32_t *__restrict__ cnt) {
+                             int chunk, int32_t *__restrict__ cnt) {
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < npar; j += (int64_t)gridDim.x * blockDim.x) {
     const int n = leaf_beg[par_leaf[j + 1]] - leaf_beg[par_leaf[j]];
-    cnt[j] = (n + 31) >> 5;
+    cnt[j] = (n + chunk - 1) / chunk;
   }
 }
 
 __global__ void k_item_fill(const int32_t *__restrict__ par_leaf, const int32_t *__restrict__ leaf_beg, int64_t npar,
-                            const int64_t *__restrict__ off, int32_t *__restrict__ item_par,
+                            int chunk, const int64_t *__restrict__ off, int32_t *__restrict__ item_par,
                             int32_t *__restrict__ item_q0) {
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < npar; j += (int64_t)gridDim.x * blockDim.x) {
     const int q0 = leaf_beg[par_leaf[j]], q1 = leaf_beg[par_leaf[j + 1]];
     int64_t o = off[j];
-    for (int q = q0; q < q1; q += 32, ++o) {
+    for (int q = q0; q < q1; q += chunk, ++o) {
       item_par[o] = (int32_t)j;
       item_q0[o] = q;
     }
+  }
+}
+
+template <int K>
+static void launch_ws(const LeafPK &la, const ItemWS &iw, const Dom &D, cudaStream_t st) {
+  const size_t smem = sizeof(WSShared);
+  if (D.periodic) {
+    JZ_CUDA(cudaFuncSetAttribute(k_leafws<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_leafws<K, true><<<(unsigned)iw.nitems, kWThreads, smem, st>>>(la, iw, D);
+  } else {
+    JZ_CUDA(cudaFuncSetAttribute(k_leafws<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_leafws<K, false><<<(unsigned)iw.nitems, kWThreads, smem, st>>>(la, iw, D);
   }
 }
 
@@ -447,14 +887,16 @@ void leaf_to_leaf(const LeafArgs &a, const Dom &D, cudaStream_t st) {
   int64_t *off = nullptr;
   JZ_CUDA(cudaMallocAsync(&cnt, a.npar * sizeof(int32_t), st));
   JZ_CUDA(cudaMallocAsync(&off, (a.npar + 1) * sizeof(int64_t), st));
-  k_item_count<<<grid_for(a.npar, 256), 256, 0, st>>>(a.par_leaf, a.leaf_beg, a.npar, cnt);
+  const bool ws = (a.flags & JZ_FLAG_WS_LEAF) != 0;  // experimental warp-specialised variant
+  const int chunk = ws ? kWC * 32 : 32;
+  k_item_count<<<grid_for(a.npar, 256), 256, 0, st>>>(a.par_leaf, a.leaf_beg, a.npar, chunk, cnt);
   JZ_LAUNCH_CHECK();
   exclusive_scan_i32_to_i64(cnt, off, a.npar, st);
   const int64_t nitems = read_i64(off + a.npar, st);
   int32_t *item_par = nullptr, *item_q0 = nullptr;
   JZ_CUDA(cudaMallocAsync(&item_par, (nitems + 1) * sizeof(int32_t), st));
   JZ_CUDA(cudaMallocAsync(&item_q0, (nitems + 1) * sizeof(int32_t), st));
-  k_item_fill<<<grid_for(a.npar, 256), 256, 0, st>>>(a.par_leaf, a.leaf_beg, a.npar, off, item_par, item_q0);
+  k_item_fill<<<grid_for(a.npar, 256), 256, 0, st>>>(a.par_leaf, a.leaf_beg, a.npar, chunk, off, item_par, item_q0);
   JZ_LAUNCH_CHECK();
 
   LeafPK la;
@@ -481,11 +923,19 @@ void leaf_to_leaf(const LeafArgs &a, const Dom &D, cudaStream_t st) {
   la.out_d2 = a.out_d2;
   la.out_row_gidx = a.out_row_gidx;
   la.stats = a.evals;
-  const unsigned blocks = (unsigned)ceil_div(nitems, kLWarps);
-  if (blocks) {
-    if (a.k <= 8) launch_l<8>(la, D, blocks, st);
-    else if (a.k <= 16) launch_l<16>(la, D, blocks, st);
-    else launch_l<32>(la, D, blocks, st);
+  la.seed_d2 = nullptr;
+  if (nitems > 0) {
+    if (ws) {
+      ItemWS iw{item_par, item_q0, nitems};
+      if (a.k <= 8) launch_ws<8>(la, iw, D, st);
+      else if (a.k <= 16) launch_ws<16>(la, iw, D, st);
+      else launch_ws<32>(la, iw, D, st);
+    } else {
+      const unsigned blocks = (unsigned)ceil_div(nitems, kLWarps);
+      if (a.k <= 8) launch_l<8>(la, D, blocks, st);
+      else if (a.k <= 16) launch_l<16>(la, D, blocks, st);
+      else launch_l<32>(la, D, blocks, st);
+    }
     JZ_LAUNCH_CHECK();
   }
   JZ_CUDA(cudaFreeAsync(cnt, st));

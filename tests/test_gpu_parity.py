@@ -120,6 +120,17 @@ def test_pruning_safety():
         assert np.array_equal(ref[0], got[0]) and np.array_equal(ref[1].view(np.int32), got[1].view(np.int32))
 
 
+@pytest.mark.parametrize("box,k", [(1.0, 16), (None, 8), (1.0, 32)])
+def test_parity_warp_specialised_variant(box, k):
+    """The experimental warp-specialised LeafToLeaf (producer warp + mbarrier ring) gives the
+    same bits as the default kernel and the oracle."""
+    jz = _jz()
+    pos = clustered_points(60000, 31, 1.0)
+    ig, dg = _gpu_knn(pos, k, box, params=dict(flags=jz.JZ_FLAG_WS_LEAF))
+    io, do = knn_grid(pos, k, box)
+    _assert_same(ig, dg, io, do)
+
+
 def test_z_order_rows():
     pos = uniform_points(20000, 9, 1.0)
     ii, di = _gpu_knn(pos, 8, 1.0)
