@@ -120,7 +120,7 @@ __device__ __forceinline__ void st_relaxed(unsigned long long *p, unsigned long 
 // ---------------------------------------------------------------- A3: one-sweep pass
 // FIRST: keys computed from positions, vals = input index.  LAST: gather float4 output.
 template <bool FIRST, bool LAST>
-__global__ void __launch_bounds__(kSortThreads) k_onesweep(
+__global__ void __launch_bounds__(kSortThreads, 3) k_onesweep(
     const float *__restrict__ pos, int stride, int gidx_mode, int64_t gidx_base, Frame f,
     const uint64_t *__restrict__ kin, const uint32_t *__restrict__ vin, uint64_t *__restrict__ kout,
     uint32_t *__restrict__ vout, float4 *__restrict__ pts_out, int64_t n, int shift,
