@@ -1,12 +1,13 @@
 // jz_build.cu -- plane-based tree hierarchy (§2.3).
 //
-//  A4 k_levels       lvl_g = bitlen(key_{g-1} xor key_g) for gaps g in [1, N-1]; lvl_0 = lvl_N = 64
-//                    (integer-key reading DESIGN.md R4/R5).
-//  A5 k_leaf_flags   gap g is a leaf split iff n_g > N_max^(0), decided inside a +-N_max^(0) window
-//                    of gap levels staged in shared memory (P:L253 step (2) "range search"). n_g is
-//                    the distance between the nearest gaps with a strictly greater level on each
-//                    side (equal to the paper's binary-search definition; pinned by
-//                    tests/test_oracle_tree.py::test_node_ranges_equal_nearest_greater).
+//  A4 levels        lvl_g = bitlen(key_{g-1} xor key_g) for gaps g in [1, N-1]; lvl_0 = lvl_N = 64
+//                    (integer-key reading DESIGN.md R4/R5), computed on the fly.
+//  A5 k_leaf_flags   gap g is a leaf split iff n_g > N_max^(0), where n_g is the size of the Morton
+//                    cell at level lvl_g holding points g-1 and g (= the distance between the
+//                    nearest gaps with a strictly greater level, = the paper's binary-search
+//                    definition; pinned by tests/test_oracle_tree.py). Decided inside a
+//                    +-N_max^(0) window of keys staged in shared memory with two binary searches
+//                    (P:L253 step (2) "range search").
 //     compaction     scan + scatter -> spl^(0).
 //  A6 k_split_n      exact n at every leaf split by the paper's two binary searches on the
 //                    sorted keys (P:L147-155, P:L253 step (3)).
@@ -24,46 +25,59 @@
 
 namespace jz {
 
-__global__ void k_levels(const uint64_t *__restrict__ keys, int64_t n, uint8_t *__restrict__ lvl) {
-  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g <= n; g += (int64_t)gridDim.x * blockDim.x) {
-    uint8_t l = kLevelSentinel;
-    if (g > 0 && g < n) l = (uint8_t)(64 - __clzll((long long)(keys[g - 1] ^ keys[g])));
-    lvl[g] = l;
-  }
-}
-
 constexpr int kFlagBlock = 512;
 
-__global__ void __launch_bounds__(kFlagBlock) k_leaf_flags(const uint8_t *__restrict__ lvl, int64_t n, int W,
+// Leaf-split test (P:L253 step (2)): gap g is a split iff the Morton cell at level
+// lvl_g = bitlen(key_{g-1} ^ key_g) holding points g-1 and g has more than W = N_max^(0) points.
+// The cell is the contiguous run of keys sharing key >> lvl_g (a node is the set of
+// points sharing the leading bits), so n <= W can be decided inside a +-W window of keys staged
+// in shared memory with two binary searches (<= 2 log2 W probes per gap).
+__global__ void __launch_bounds__(kFlagBlock) k_leaf_flags(const uint64_t *__restrict__ keys, int64_t n, int W,
                                                            int32_t *__restrict__ flag) {
-  extern __shared__ uint8_t s_l[];
+  extern __shared__ uint64_t s_k[];
   const int64_t b0 = (int64_t)blockIdx.x * kFlagBlock;
-  const int64_t w0 = b0 - W;
+  const int64_t w0 = b0 - W - 1;
   const int len = kFlagBlock + 2 * W + 2;
   for (int i = threadIdx.x; i < len; i += blockDim.x) {
-    int64_t g = w0 + i;
-    s_l[i] = (g < 0 || g > n) ? (uint8_t)255 : lvl[g];
+    const int64_t g = w0 + i;
+    s_k[i] = (g < 0 || g >= n) ? 0ull : keys[g];
   }
   __syncthreads();
   const int64_t g = b0 + threadIdx.x;
   if (g > n) return;
   int f = 1;
   if (g > 0 && g < n) {
-    const int li = s_l[g - w0];
-    int64_t L = -1;
-    for (int64_t j = g - 1; j >= g + 1 - W; --j)
-      if (s_l[j - w0] > li) {
-        L = j;
-        break;
+    const uint64_t kg = s_k[g - w0], kg1 = s_k[g - 1 - w0];
+    const int l = 64 - __clzll((long long)(kg1 ^ kg));
+    const uint64_t p = l >= 64 ? 0ull : (kg >> l);
+    auto pre = [&](int64_t i) { return l >= 64 ? 0ull : (s_k[i - w0] >> l); };
+    // L_b: first index of the cell; if it starts before g - W the cell has > W points
+    const int64_t lo_lim = g - W > 0 ? g - W : 0;
+    if (!(g - W >= 1 && pre(g - W) == p)) {
+      int64_t lo = lo_lim, hi = g - 1;  // smallest a in [lo, g-1] with prefix == p (true at g-1)
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (pre(mid) == p) hi = mid;
+        else lo = mid + 1;
       }
-    if (L >= 0) {
-      int64_t R = -1;
-      for (int64_t j = g + 1; j <= L + W; ++j)
-        if (s_l[j - w0] > li) {
-          R = j;
-          break;
+      const int64_t Lb = lo;
+      // R_b: first index after the cell; n = R_b - L_b <= W iff R_b <= L_b + W
+      const int64_t rmax = Lb + W < n ? Lb + W : n;  // R_b = n if the cell reaches the end
+      if (rmax >= n) {
+        f = (n - Lb) > W;
+        if (f == 0) {
+          // the cell ends at n only if every key up to n-1 shares the prefix
+          int64_t lo2 = g, hi2 = n;
+          while (lo2 < hi2) {
+            const int64_t mid = (lo2 + hi2) >> 1;
+            if (pre(mid) != p) hi2 = mid;
+            else lo2 = mid + 1;
+          }
+          f = (lo2 - Lb) > W;
         }
-      f = R < 0;  // found within the window <=> n = R - L <= N_max^(0)
+      } else {
+        f = pre(rmax) == p;  // cell still continues at L_b + W => n > W
+      }
     }
   }
   flag[g] = f;
@@ -77,15 +91,15 @@ __global__ void k_compact_gaps(const int32_t *__restrict__ flag, const int64_t *
 
 // n at every leaf split by binary search on keys.
 __global__ void k_split_n(const uint64_t *__restrict__ keys, int64_t n, const int32_t *__restrict__ spl,
-                          int64_t nspl, const uint8_t *__restrict__ lvl, int32_t *__restrict__ nsplit) {
+                          int64_t nspl, int32_t *__restrict__ nsplit) {
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nspl; j += (int64_t)gridDim.x * blockDim.x) {
     const int64_t g = spl[j];
     if (g <= 0 || g >= n) {
       nsplit[j] = INT_MAX;
       continue;
     }
-    const int l = lvl[g];
     const uint64_t kg = keys[g], kg1 = keys[g - 1];
+    const int l = 64 - __clzll((long long)(kg1 ^ kg));
     // l_b: smallest a in [0, g-1] with bitlen(key_a ^ key_g) <= l
     int64_t lo = 0, hi = g - 1;
     while (lo < hi) {
@@ -217,16 +231,12 @@ void free_planes(std::vector<Plane> &planes, cudaStream_t st) {
 void build_planes(const uint64_t *keys, const float4 *pts, int64_t n, const jz_knn_params_t &prm,
                   std::vector<Plane> &planes, cudaStream_t st) {
   const int W = prm.nmax0;
-  uint8_t *lvl = nullptr;
   int32_t *flag = nullptr;
   int64_t *pos = nullptr;
-  JZ_CUDA(cudaMallocAsync(&lvl, (n + 1) * sizeof(uint8_t), st));
   JZ_CUDA(cudaMallocAsync(&flag, (n + 1) * sizeof(int32_t), st));
   JZ_CUDA(cudaMallocAsync(&pos, (n + 2) * sizeof(int64_t), st));
-  k_levels<<<grid_for(n + 1, 256), 256, 0, st>>>(keys, n, lvl);
-  JZ_LAUNCH_CHECK();
   const unsigned fb = (unsigned)ceil_div(n + 1, kFlagBlock);
-  k_leaf_flags<<<fb, kFlagBlock, kFlagBlock + 2 * W + 2, st>>>(lvl, n, W, flag);
+  k_leaf_flags<<<fb, kFlagBlock, (kFlagBlock + 2 * W + 2) * sizeof(uint64_t), st>>>(keys, n, W, flag);
   JZ_LAUNCH_CHECK();
   exclusive_scan_i32_to_i64(flag, pos, n + 1, st);
   const int64_t nspl = read_i64(pos + (n + 1), st);  // = N_leaf + 1
@@ -242,7 +252,7 @@ void build_planes(const uint64_t *keys, const float4 *pts, int64_t n, const jz_k
   JZ_LAUNCH_CHECK();
   int32_t *nsplit = nullptr;
   JZ_CUDA(cudaMallocAsync(&nsplit, nspl * sizeof(int32_t), st));
-  k_split_n<<<grid_for(nspl, 128), 128, 0, st>>>(keys, n, leaf.beg, nspl, lvl, nsplit);
+  k_split_n<<<grid_for(nspl, 128), 128, 0, st>>>(keys, n, leaf.beg, nspl, nsplit);
   JZ_LAUNCH_CHECK();
   k_leaf_boxes<<<grid_for(leaf.nnodes * 32, 256), 256, 0, st>>>(pts, leaf.beg, leaf.nnodes, leaf.box);
   JZ_LAUNCH_CHECK();
@@ -272,7 +282,6 @@ void build_planes(const uint64_t *keys, const float4 *pts, int64_t n, const jz_k
     planes.push_back(pl);
   }
   JZ_CUDA(cudaFreeAsync(nsplit, st));
-  JZ_CUDA(cudaFreeAsync(lvl, st));
   JZ_CUDA(cudaFreeAsync(flag, st));
   JZ_CUDA(cudaFreeAsync(pos, st));
 }
