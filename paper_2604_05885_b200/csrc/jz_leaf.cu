@@ -25,7 +25,7 @@
 
 namespace jz {
 
-constexpr int kLWarps = 4;
+constexpr int kLWarps = 2;
 constexpr int kLThreads = kLWarps * 32;
 constexpr int kLCap = 256;  // staged source points per warp (4 KB SoA)
 constexpr int kQCap = 16;   // per-lane candidate queue (4 KB per warp)
