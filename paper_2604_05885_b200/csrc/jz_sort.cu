@@ -121,7 +121,7 @@ __device__ __forceinline__ void st_relaxed(unsigned long long *p, unsigned long 
 // FIRST: keys computed from positions, vals = input index.  LAST: gather float4 output.
 template <bool FIRST, bool LAST>
 __global__ void __launch_bounds__(kSortThreads, 3) k_onesweep(
-    const float *__restrict__ pos, int stride, int gidx_mode, int64_t gidx_base, Frame f,
+    const float *__restrict__ pos, int stride, int gidx_mode, int64_t gidx_base, Frame f, float4 *__restrict__ pos4,
     const uint64_t *__restrict__ kin, const uint32_t *__restrict__ vin, uint64_t *__restrict__ kout,
     uint32_t *__restrict__ vout, float4 *__restrict__ pts_out, int64_t n, int shift,
     const unsigned int *__restrict__ digit_base, unsigned long long *status, int *tile_counter) {
@@ -150,6 +150,8 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_onesweep(
         const float *p = pos + idx * stride;
         key[i] = morton(p[0], p[1], p[2], f);
         val[i] = (uint32_t)idx;
+        // aligned float4 copy {x, y, z, bits(gidx)} for the final gather (one 16-byte load per point)
+        if (pos4) pos4[idx] = make_float4(p[0], p[1], p[2], __int_as_float((int)(gidx_base + idx)));
       } else {
         key[i] = kin[idx];
         val[i] = vin[idx];
@@ -236,9 +238,14 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_onesweep(
     kout[gp] = k;
     vout[gp] = v;
     if (LAST) {
-      const float *p = pos + (int64_t)v * stride;
-      int g = gidx_mode ? __float_as_int(p[3]) : (int)(gidx_base + v);
-      pts_out[gp] = make_float4(p[0], p[1], p[2], __int_as_float(g));
+      if (gidx_mode) {
+        pts_out[gp] = reinterpret_cast<const float4 *>(pos)[v];  // input rows are float4 {x, y, z, gidx}
+      } else if (pos4 && !FIRST) {
+        pts_out[gp] = pos4[v];
+      } else {
+        const float *p = pos + (int64_t)v * stride;
+        pts_out[gp] = make_float4(p[0], p[1], p[2], __int_as_float((int)(gidx_base + v)));
+      }
     }
   }
 }
@@ -330,6 +337,8 @@ void sort_points(const float *pos, int64_t n, int stride, int gidx_mode, int64_t
   JZ_CUDA(cudaMallocAsync(&kbuf[0], n * sizeof(uint64_t), st));
   JZ_CUDA(cudaMallocAsync(&vbuf[0], n * sizeof(uint32_t), st));
   const int np = (int)passes.size();
+  float4 *pos4 = nullptr;  // aligned float4 copy written by the first pass (xyz input, >= 2 passes)
+  if (!gidx_mode && np > 1) JZ_CUDA(cudaMallocAsync(&pos4, n * sizeof(float4), st));
   if (np > 1) {
     JZ_CUDA(cudaMallocAsync(&kbuf[1], n * sizeof(uint64_t), st));
     JZ_CUDA(cudaMallocAsync(&vbuf[1], n * sizeof(uint32_t), st));
@@ -346,7 +355,7 @@ void sort_points(const float *pos, int64_t n, int stride, int gidx_mode, int64_t
     int *tc = counters + i;
     dim3 g((unsigned)ntiles);
 #define JZ_PASS(F, L)                                                                                          \
-  k_onesweep<F, L><<<g, kSortThreads, 0, st>>>(pos, stride, gidx_mode, gidx_base, frame, ki, vi, ko, vo, pts_out, \
+  k_onesweep<F, L><<<g, kSortThreads, 0, st>>>(pos, stride, gidx_mode, gidx_base, frame, pos4, ki, vi, ko, vo, pts_out, \
                                                n, 8 * p, db, status, tc)
     if (first && last) JZ_PASS(true, true);
     else if (first) JZ_PASS(true, false);
@@ -357,6 +366,7 @@ void sort_points(const float *pos, int64_t n, int stride, int gidx_mode, int64_t
   }
   JZ_CUDA(cudaFreeAsync(status, st));
   JZ_CUDA(cudaFreeAsync(counters, st));
+  if (pos4) JZ_CUDA(cudaFreeAsync(pos4, st));
   JZ_CUDA(cudaFreeAsync(kbuf[0], st));
   JZ_CUDA(cudaFreeAsync(vbuf[0], st));
   if (kbuf[1]) JZ_CUDA(cudaFreeAsync(kbuf[1], st));
