@@ -26,6 +26,12 @@
  *                      returns the same bits (pinned against brute in tests).
  * Both may run a subset of query rows (rows != NULL) for sampled checks.
  *
+ * Separate query points ("query the tree using a set of query points
+ * x_query distinct from the source points x"): the *_q entry
+ * points take a query array; row r is then the k smallest (d2(x_query[i], x_j), j)
+ * over the sources j, i = rows ? rows[r] : r. Any k <= N works (PAPER.md L386:
+ * k > k_max is the kernel's business, not the definition's).
+ *
  * Build: gcc -O2 -fopenmp -ffp-contract=off -fPIC -shared (no -ffast-math).
  */
 #include <math.h>
@@ -126,16 +132,16 @@ int oracle_max_threads(void) {
  * Brute force: rows r in [0, nrows) query point q = rows ? rows[r] : r.
  * out_idx/out_d2 are [nrows][k] row-major. Returns 0, or 2 on bad args.
  */
-int oracle_knn_brute(const float *pos, int64_t n, const float *box, int k, const int64_t *rows,
-                     int64_t nrows, int32_t *out_idx, float *out_d2, int nthreads) {
-  if (n < 1 || k < 1 || k > n) return 2;
+int oracle_knn_brute_q(const float *pos, int64_t n, const float *qry, const float *box, int k,
+                       const int64_t *rows, int64_t nrows, int32_t *out_idx, float *out_d2, int nthreads) {
+  if (n < 1 || k < 1 || k > n || !qry) return 2;
   domain_t dom;
   make_domain(&dom, box);
   set_threads(nthreads);
 #pragma omp parallel for schedule(dynamic, 64)
   for (int64_t r = 0; r < nrows; ++r) {
     int64_t i = rows ? rows[r] : r;
-    const float *q = pos + 3 * i;
+    const float *q = qry + 3 * i;
     topk_t t = {k, 0, out_d2 + r * k, out_idx + r * k};
     for (int64_t j = 0; j < n; ++j) {
       float d2 = canon_d2(q, pos + 3 * j, &dom);
@@ -144,6 +150,12 @@ int oracle_knn_brute(const float *pos, int64_t n, const float *box, int k, const
     }
   }
   return 0;
+}
+
+/* Self-query: the query points are the sources. */
+int oracle_knn_brute(const float *pos, int64_t n, const float *box, int k, const int64_t *rows,
+                     int64_t nrows, int32_t *out_idx, float *out_d2, int nthreads) {
+  return oracle_knn_brute_q(pos, n, pos, box, k, rows, nrows, out_idx, out_d2, nthreads);
 }
 
 /* ------------------------------------------------------------------------- */
@@ -310,9 +322,9 @@ static void grid_query(const grid_t *g, const float *pos, const float *q, const 
   }
 }
 
-int oracle_knn_grid(const float *pos, int64_t n, const float *box, int k, const int64_t *rows, int64_t nrows,
-                    int32_t *out_idx, float *out_d2, int nthreads, double per_cell) {
-  if (n < 1 || k < 1 || k > n) return 2;
+int oracle_knn_grid_q(const float *pos, int64_t n, const float *qry, const float *box, int k, const int64_t *rows,
+                      int64_t nrows, int32_t *out_idx, float *out_d2, int nthreads, double per_cell) {
+  if (n < 1 || k < 1 || k > n || !qry) return 2;
   domain_t dom;
   make_domain(&dom, box);
   set_threads(nthreads);
@@ -327,10 +339,15 @@ int oracle_knn_grid(const float *pos, int64_t n, const float *box, int k, const 
   for (int64_t r = 0; r < nrows; ++r) {
     int64_t i = rows ? rows[r] : r;
     topk_t t = {k, 0, out_d2 + r * k, out_idx + r * k};
-    grid_query(&g, pos, pos + 3 * i, &dom, &t);
+    grid_query(&g, pos, qry + 3 * i, &dom, &t);
   }
   grid_free(&g);
   return 0;
+}
+
+int oracle_knn_grid(const float *pos, int64_t n, const float *box, int k, const int64_t *rows, int64_t nrows,
+                    int32_t *out_idx, float *out_d2, int nthreads, double per_cell) {
+  return oracle_knn_grid_q(pos, n, pos, box, k, rows, nrows, out_idx, out_d2, nthreads, per_cell);
 }
 
 /* Canonical d2 of explicit pairs (for invariant tests: symmetry, stored-d2 recomputation). */

@@ -45,6 +45,12 @@ def _load():
             lib.oracle_knn_grid.argtypes = [P, ctypes.c_int64, P, ctypes.c_int, P, ctypes.c_int64, P, P,
                                             ctypes.c_int, ctypes.c_double]
             lib.oracle_knn_grid.restype = ctypes.c_int
+            lib.oracle_knn_brute_q.argtypes = [P, ctypes.c_int64, P, P, ctypes.c_int, P, ctypes.c_int64, P, P,
+                                               ctypes.c_int]
+            lib.oracle_knn_brute_q.restype = ctypes.c_int
+            lib.oracle_knn_grid_q.argtypes = [P, ctypes.c_int64, P, P, ctypes.c_int, P, ctypes.c_int64, P, P,
+                                              ctypes.c_int, ctypes.c_double]
+            lib.oracle_knn_grid_q.restype = ctypes.c_int
             lib.oracle_pair_d2.argtypes = [P, P, ctypes.c_int64, P, P]
             lib.oracle_pair_d2.restype = None
             lib.oracle_max_threads.argtypes = []
@@ -71,30 +77,46 @@ def _ptr(a):
     return None if a is None else a.ctypes.data
 
 
-def _run(fn, pos, k, box, rows, threads, *extra):
+def _run(fn, pos, k, box, rows, threads, *extra, queries=None):
     pos, b = _prep(pos, box)
     n = pos.shape[0]
+    qry = None
+    if queries is not None:
+        qry, _ = _prep(queries, None)
     if rows is None:
-        nrows, r = n, None
+        nrows, r = (n if qry is None else qry.shape[0]), None
     else:
         r = np.ascontiguousarray(rows, dtype=np.int64)
         nrows = r.shape[0]
     idx = np.empty((nrows, k), dtype=np.int32)
     d2 = np.empty((nrows, k), dtype=np.float32)
-    rc = fn(_ptr(pos), n, _ptr(b), int(k), _ptr(r), nrows, _ptr(idx), _ptr(d2), int(threads or 0), *extra)
+    if qry is None:
+        rc = fn(_ptr(pos), n, _ptr(b), int(k), _ptr(r), nrows, _ptr(idx), _ptr(d2), int(threads or 0), *extra)
+    else:
+        rc = fn(_ptr(pos), n, _ptr(qry), _ptr(b), int(k), _ptr(r), nrows, _ptr(idx), _ptr(d2), int(threads or 0),
+                *extra)
     if rc != 0:
         raise ValueError(f"oracle returned status {rc} (n={n}, k={k})")
     return idx, d2
 
 
-def knn_brute(pos, k: int, box=None, rows=None, threads: int | None = None):
-    """O(N^2) definition. Returns (idx int32 [m,k], d2 float32 [m,k])."""
-    return _run(_load().oracle_knn_brute, pos, k, box, rows, threads)
+def knn_brute(pos, k: int, box=None, rows=None, threads: int | None = None, queries=None):
+    """O(N^2) definition. Returns (idx int32 [m,k], d2 float32 [m,k]).
+
+    queries=None: self-query. Otherwise row i answers queries[i] against
+    the sources `pos` (separate query points)."""
+    lib = _load()
+    if queries is None:
+        return _run(lib.oracle_knn_brute, pos, k, box, rows, threads)
+    return _run(lib.oracle_knn_brute_q, pos, k, box, rows, threads, queries=queries)
 
 
-def knn_grid(pos, k: int, box=None, rows=None, threads: int | None = None, per_cell: float = 2.0):
+def knn_grid(pos, k: int, box=None, rows=None, threads: int | None = None, per_cell: float = 2.0, queries=None):
     """Uniform-grid shell search, same bits as knn_brute."""
-    return _run(_load().oracle_knn_grid, pos, k, box, rows, threads, ctypes.c_double(per_cell))
+    lib = _load()
+    if queries is None:
+        return _run(lib.oracle_knn_grid, pos, k, box, rows, threads, ctypes.c_double(per_cell))
+    return _run(lib.oracle_knn_grid_q, pos, k, box, rows, threads, ctypes.c_double(per_cell), queries=queries)
 
 
 def pair_d2(a, b, box=None):

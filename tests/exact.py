@@ -56,11 +56,13 @@ def to_f32(x: Fraction) -> np.float32:
     return np.float32(float(x))
 
 
-def brute_exact(pos, k, box=None):
-    """Pure-Python definition on tiny inputs: rows of (j, d2) sorted by (d2, j)."""
+def brute_exact(pos, k, box=None, queries=None):
+    """Pure-Python definition on tiny inputs: rows of (j, d2) sorted by (d2, j).
+    queries=None: self-query; else row i answers queries[i] against the sources pos."""
     n = len(pos)
+    qs = pos if queries is None else queries
     rows = []
-    for i in range(n):
-        cand = sorted((canon_d2_exact(pos[i], pos[j], box), j) for j in range(n))
+    for i in range(len(qs)):
+        cand = sorted((canon_d2_exact(qs[i], pos[j], box), j) for j in range(n))
         rows.append([(j, to_f32(d)) for d, j in cand[:k]])
     return rows

@@ -250,3 +250,70 @@ def test_scipy_ckdtree_crosscheck(box):
     for i in mismatch:  # allowed only for a near-tie at the k-th place
         assert abs(dd[i, k] - dd[i, k - 1]) <= 2 * tol[i, k - 1]
     assert len(mismatch) <= 5
+
+
+# --------------------------------------------------------------------------- separate queries, k > 32
+# query points distinct from the sources and k > k_max
+# (PAPER.md L386). The definition is unchanged: row i = k smallest (d2(x_query_i, x_j), j).
+
+
+@pytest.mark.parametrize("box", [None, 1.0, (0.75, 1.0, 1.25)])
+def test_brute_q_equals_exact_rational_definition(box):
+    L = np.broadcast_to(np.asarray(1.0 if box is None else box, dtype=np.float32), (3,))
+    src = (_rand_f32(30, 81) * L).astype(np.float32)
+    qry = (_rand_f32(23, 82) * L).astype(np.float32)
+    if box is None:
+        qry = (qry * np.float32(1.6) - np.float32(0.3)).astype(np.float32)  # some outside the source hull
+    src = np.where(src >= L, 0, src).astype(np.float32)
+    qry = np.where(qry >= L, 0, qry).astype(np.float32) if box is not None else qry
+    k = 9
+    idx, d2 = knn_brute(src, k, box, queries=qry)
+    ref = brute_exact(src, k, box, queries=qry)
+    assert idx.shape == (23, k)
+    for i in range(len(qry)):
+        assert [j for j, _ in ref[i]] == list(idx[i])
+        assert np.array_equal(np.array([d for _, d in ref[i]], dtype=np.float32).view(np.int32), d2[i].view(np.int32))
+
+
+def _q_sets():
+    yield "uniform", uniform_points(3000, 91, 1.0), uniform_points(1700, 92, 1.0), 1.0
+    yield "clustered-src-uniform-q", clustered_points(4000, 93, 1.0), uniform_points(2500, 94, 1.0), 1.0
+    yield "uniform-src-clustered-q", uniform_points(2000, 95, 1.0), clustered_points(5000, 96, 1.0), 1.0
+    yield "open-q-outside-hull", uniform_points(2000, 97, 1.0), (uniform_points(800, 98, 1.0) * 3 - 1), None
+    yield "few-q", clustered_points(5000, 99, 1.0), uniform_points(7, 100, 1.0), None
+    yield "lattice-ties", lattice_points(8, 0.125), lattice_points(4, 0.25) + np.float32(0.0625), 1.0
+
+
+@pytest.mark.parametrize("name,src,qry,box", list(_q_sets()), ids=[s[0] for s in _q_sets()])
+@pytest.mark.parametrize("k", [1, 16, 100])
+def test_grid_q_equals_brute_q(name, src, qry, box, k):
+    i1, d1 = knn_brute(src, k, box, queries=qry)
+    i2, d2 = knn_grid(src, k, box, queries=qry)
+    assert i1.shape == (len(qry), k)
+    assert np.array_equal(i1, i2)
+    assert np.array_equal(d1.view(np.int32), d2.view(np.int32))
+
+
+def test_queries_that_are_sources_reproduce_self_rows():
+    """A query set made of some source points (any order) gives exactly those self-query rows."""
+    src = clustered_points(6000, 101, 1.0)
+    sel = np.random.default_rng(3).choice(6000, 500, replace=False)
+    for box in (None, 1.0):
+        i_self, d_self = knn_grid(src, 24, box, rows=sel)
+        i_q, d_q = knn_brute(src, 24, box, queries=src[sel])
+        assert np.array_equal(i_self, i_q) and np.array_equal(d_self, d_q)
+
+
+def test_large_k_prefix_and_scipy():
+    """k > 32: prefix property against k = 32 and a cKDTree cross-check."""
+    from scipy.spatial import cKDTree
+
+    src = clustered_points(8000, 102, 1.0)
+    qry = uniform_points(1000, 103, 1.0)
+    i100, d100 = knn_grid(src, 100, 1.0, queries=qry)
+    i32, d32 = knn_grid(src, 32, 1.0, queries=qry)
+    assert np.array_equal(i100[:, :32], i32) and np.array_equal(d100[:, :32], d32)
+    assert np.all(np.diff(d100.astype(np.float64), axis=1) >= 0)
+    dd, _ = cKDTree(src.astype(np.float64), boxsize=1.0).query(qry.astype(np.float64), k=100)
+    tol = 1e-6 * dd + np.sqrt(3.0) * 2.0 ** -25 + 1e-30
+    assert np.all(np.abs(np.sqrt(d100.astype(np.float64)) - dd) <= tol)
