@@ -47,7 +47,7 @@ typedef struct jz_knn_index jz_knn_index;  /* opaque; owns all its device memory
 
 enum {
   JZ_OK = 0,
-  JZ_EINVAL = 2,    /* bad argument (n < 1, k < 1, k > n, k > 32, bad box, bad order, NULL pointer) */
+  JZ_EINVAL = 2,    /* bad argument (n < 1, k < 1, k > number of sources, bad box, bad order, NULL pointer) */
   JZ_EDATA = 3,     /* NaN / Inf coordinate, or periodic coordinate outside [0, L) */
   JZ_ECAPACITY = 4, /* reserved: internal capacities grow on demand */
   JZ_ECUDA = 5,     /* CUDA runtime error (message in jz_last_error) */
@@ -59,8 +59,7 @@ enum { JZ_ORDER_INPUT = 0, JZ_ORDER_Z = 1 };
 enum {
   JZ_FLAG_FRAME = 1u << 0,         /* use frame_origin / frame_extent for the Morton keys (multi-GPU: one global frame) */
   JZ_FLAG_NO_EARLY_EXIT = 1u << 1, /* disable the sorted-r_low early exit (pruning-safety tests) */
-  JZ_FLAG_NO_SEGSORT = 1u << 2,    /* do not sort interaction segments by r_low (implies no early exit) */
-  JZ_FLAG_WS_LEAF = 1u << 13       /* experimental: warp-specialised LeafToLeaf (producer warp + mbarrier ring) */
+  JZ_FLAG_NO_SEGSORT = 1u << 2     /* do not sort interaction segments by r_low (implies no early exit) */
 };
 
 /* Tree / walk parameters. Zero fields take the defaults (nmax0 see DESIGN.md §6). */
@@ -90,22 +89,44 @@ JZ_API int jz_knn_build(const float *pos, int64_t n, const float *box, const jz_
 
 /*
  * Build over points that carry their global index: pts4[i] = {x, y, z, bits(gidx)}
- * (device, float4, gidx an int32 stored bitwise in .w). Only the first n_query
- * points (in input order) are queries; points [n_query, n) are sources only
- * (multi-GPU ghosts). jz_knn_rows() returns n_query.
+ * (device, float4, gidx an int32 stored bitwise in .w). Point types (PAPER.md L272-279
+ * "Multiple point types": one tree built jointly over all types, then type-specific
+ * z-ordered arrays with per-type leaf splits):
+ *   - query  iff its input position i < n_query (row i of the result);
+ *   - source iff gidx >= 0 (a neighbour candidate, reported as gidx).
+ * Points [n_query, n) with gidx >= 0 are sources only (multi-GPU ghosts, DESIGN.md
+ * "Multi-GPU"); points with gidx < 0 are queries only. Node counts of the walk count
+ * sources. jz_knn_rows() returns n_query.
  */
 JZ_API int jz_knn_build_xyzg(const float *pts4, int64_t n, int64_t n_query, const float *box, const jz_knn_params *p,
                       jz_stream_t s, jz_knn_index **out);
+
+/*
+ * Separate query points ("query the tree using a set of query points
+ * x_query distinct from the source points x"):
+ *   src [n_src][3], qry [n_qry][3] float (device, may be freed after the call).
+ * Builds the joint tree (L276-279) over both sets. Row i of jz_knn_query answers
+ * qry[i]; indices refer to src. n_src >= 1, n_qry >= 0, n_src + n_qry <= 2^31 - 2;
+ * periodic: all coordinates in [0, L) (JZ_EDATA otherwise). With JZ_ORDER_Z,
+ * out_row_gidx[r] = the query's row i.
+ */
+JZ_API int jz_knn_build_xq(const float *src, int64_t n_src, const float *qry, int64_t n_qry, const float *box,
+                    const jz_knn_params *p, jz_stream_t s, jz_knn_index **out);
 
 /* Number of result rows the index produces (host out). */
 JZ_API int jz_knn_rows(const jz_knn_index *ix, int64_t *m);
 
 /*
  * k nearest neighbours of every query point.
- *   k        1 <= k <= min(32, n)   (k_max = 32)
+ *   k        1 <= k <= number of sources. k > k_max = 32 runs ceil(k/32) LeafToLeaf
+ *            passes, pass c keeping only pairs after the last (d2, index) of pass c-1
+ *            ("call the kernel multiple times if k > k_max, filtering
+ *            additionally by a minimum radius R_min (and an equality breaking index
+ *            offset)").
  *   order    JZ_ORDER_INPUT: row i belongs to query point i (input position; for
  *            jz_knn_build_xyzg: the i-th query point of pts4).
- *            JZ_ORDER_Z: rows in Morton order; out_row_gidx[r] names the point.
+ *            JZ_ORDER_Z: rows in Morton order; out_row_gidx[r] names the point (its
+ *            gidx if it is also a source, else its query row).
  *   out_idx  [m][k] int32 global indices (device)
  *   out_d2   [m][k] float canonical squared distances (device)
  *   out_row_gidx [m] int32 (device) or NULL; required for JZ_ORDER_Z.
@@ -120,7 +141,7 @@ JZ_API void jz_knn_free(jz_knn_index *ix);
 /*
  * End-to-end convenience on HOST buffers: copies pos_host to the device, builds,
  * queries, copies the rows back (input order), frees. pos_host [n][3],
- * idx_host [n][k], d2_host [n][k]; pinned host memory gives full PCIe speed.
+ * idx_host [n][k], d2_host [n][k], 1 <= k <= n; pinned host memory gives full PCIe speed.
  */
 JZ_API int jz_knn_search_host(const float *pos_host, int64_t n, const float *box, const jz_knn_params *p, int k,
                        int32_t *idx_host, float *d2_host, jz_stream_t s);

@@ -8,6 +8,8 @@
     ix = jz.KnnIndex(pos, box=1.0)                 # build once (§2)
     idx, d2 = ix.query(16)                         # query many k (§3)
     idx, d2, gidx = ix.query(16, order="z")        # z-order rows + their global ids
+    idx, d2 = jz.knn(src, k=16, queries=qry)       # separate query points
+    idx, d2 = ix.query(100)                        # k > 32: ceil(k/32) LeafToLeaf passes
 
 All compute runs in the library's sm_100a kernels; PyTorch only provides device
 memory and the stream. See include/jz_knn.h for the C ABI.
@@ -20,7 +22,7 @@ import numpy as np
 import torch
 
 from . import _binding as B
-from ._binding import JzError, JZ_FLAG_FRAME, JZ_FLAG_NO_EARLY_EXIT, JZ_FLAG_NO_SEGSORT, JZ_FLAG_WS_LEAF  # noqa: F401
+from ._binding import JzError, JZ_FLAG_FRAME, JZ_FLAG_NO_EARLY_EXIT, JZ_FLAG_NO_SEGSORT  # noqa: F401
 
 __all__ = ["KnnIndex", "knn", "knn_host", "JzError", "set_timing"]
 
@@ -30,9 +32,12 @@ def set_timing(on: bool = True):
 
 
 class KnnIndex:
-    """Tree over `pos` (CUDA float32 [n,3], or [n,4] {x,y,z,bits(gidx)} with n_query)."""
+    """Tree over `pos` (CUDA float32 [n,3], or [n,4] {x,y,z,bits(gidx)} with n_query; a
+    negative gidx marks a query-only point). With `queries` ([m,3]) the tree is built jointly
+    over sources `pos` and the queries and row i answers queries[i]."""
 
-    def __init__(self, pos: torch.Tensor, box=None, params=None, n_query: int | None = None, stream=None):
+    def __init__(self, pos: torch.Tensor, box=None, params=None, n_query: int | None = None, stream=None,
+                 queries: torch.Tensor | None = None):
         if not (isinstance(pos, torch.Tensor) and pos.is_cuda and pos.dtype == torch.float32):
             raise TypeError("pos must be a CUDA float32 tensor")
         pos = pos.contiguous()
@@ -42,7 +47,16 @@ class KnnIndex:
         self.stream = stream
         prm = B.make_params(params)
         st = B.stream_ptr(stream)
-        if pos.dim() == 2 and pos.shape[1] == 3:
+        if queries is not None:
+            if not (isinstance(queries, torch.Tensor) and queries.is_cuda and queries.dtype == torch.float32
+                    and queries.dim() == 2 and queries.shape[1] == 3 and pos.dim() == 2 and pos.shape[1] == 3):
+                raise TypeError("pos and queries must be CUDA float32 [n,3] tensors")
+            if n_query is not None:
+                raise ValueError("n_query and queries are exclusive")
+            queries = queries.contiguous()
+            B.check(self._lib.jz_knn_build_xq(B.dptr(pos), pos.shape[0], B.dptr(queries), queries.shape[0],
+                                              B.box3(box), ctypes.byref(prm), st, ctypes.byref(self._h)))
+        elif pos.dim() == 2 and pos.shape[1] == 3:
             if n_query is not None and n_query != pos.shape[0]:
                 raise ValueError("n_query needs [n,4] xyzg input")
             B.check(self._lib.jz_knn_build(B.dptr(pos), pos.shape[0], B.box3(box), ctypes.byref(prm), st,
@@ -130,9 +144,10 @@ class KnnIndex:
             pass
 
 
-def knn(pos: torch.Tensor, k: int, box=None, order: str = "input", params=None, stream=None):
-    """Exact kNN of every point of `pos` among all points (self included)."""
-    ix = KnnIndex(pos, box=box, params=params, stream=stream)
+def knn(pos: torch.Tensor, k: int, box=None, order: str = "input", params=None, stream=None, queries=None):
+    """Exact kNN of every point of `pos` among all points (self included), or of every row of
+    `queries` among the points of `pos`."""
+    ix = KnnIndex(pos, box=box, params=params, stream=stream, queries=queries)
     try:
         return ix.query(k, order=order)
     finally:

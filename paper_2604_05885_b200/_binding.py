@@ -14,11 +14,11 @@ LIB_PATH = os.path.join(_HERE, "libjzknn.so")
 
 JZ_OK, JZ_EINVAL, JZ_EDATA, JZ_ECAPACITY, JZ_ECUDA, JZ_ENOMEM = 0, 2, 3, 4, 5, 7
 JZ_ORDER_INPUT, JZ_ORDER_Z = 0, 1
-JZ_FLAG_FRAME, JZ_FLAG_NO_EARLY_EXIT, JZ_FLAG_NO_SEGSORT, JZ_FLAG_WS_LEAF = 1, 2, 4, 1 << 13
+JZ_FLAG_FRAME, JZ_FLAG_NO_EARLY_EXIT, JZ_FLAG_NO_SEGSORT = 1, 2, 4
 
 # every symbol include/jz_knn.h declares (tests check the library exports them all)
 EXPORTS = [
-    "jz_knn_build", "jz_knn_build_xyzg", "jz_knn_rows", "jz_knn_query", "jz_knn_free", "jz_knn_search_host",
+    "jz_knn_build", "jz_knn_build_xyzg", "jz_knn_build_xq", "jz_knn_rows", "jz_knn_query", "jz_knn_free", "jz_knn_search_host",
     "jz_knn_stage_times", "jz_set_timing", "jz_last_error", "jz_morton_keys", "jz_bucket_by_splitters",
     "jz_pack_by_rank", "jz_knn_plane_nodes", "jz_knn_query_boxes", "jz_knn_select_ghosts", "jz_knn_pack_ghosts",
     "jz_knn_debug_copy", "jz_launch_count", "jz_knn_stats",
@@ -59,6 +59,7 @@ def lib():
         sig = {
             "jz_knn_build": ([P, I64, P, P, P, P], ctypes.c_int),
             "jz_knn_build_xyzg": ([P, I64, I64, P, P, P, P], ctypes.c_int),
+            "jz_knn_build_xq": ([P, I64, P, I64, P, P, P, P], ctypes.c_int),
             "jz_knn_rows": ([P, P], ctypes.c_int),
             "jz_knn_query": ([P, ctypes.c_int, ctypes.c_int, P, P, P, P], ctypes.c_int),
             "jz_knn_free": ([P], None),

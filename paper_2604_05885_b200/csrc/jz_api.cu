@@ -15,13 +15,16 @@
 
 struct jz_knn_index {
   cudaStream_t st = nullptr;
-  int64_t n = 0, n_query = 0;
+  int64_t n = 0, n_query = 0, n_src = 0;
   jz::Dom D{};
   jz_knn_params prm{};
-  float4 *pts = nullptr;
+  float4 *pts = nullptr;     // all points, z order (.w = gidx; < 0: query-only point)
   uint64_t *keys = nullptr;
-  int32_t *perm = nullptr;
-  int32_t *zrow = nullptr;
+  int32_t *perm = nullptr;   // z position -> input position
+  // type-separated views: alias pts / leaf beg / perm when every point is both
+  float4 *spts = nullptr, *qpts = nullptr;
+  int32_t *sbeg = nullptr, *qbeg = nullptr, *qin = nullptr;
+  bool own_s = false, own_q = false;
   std::vector<jz::Plane> planes;
   cudaEvent_t ev[8] = {};
   bool timing = false;
@@ -105,13 +108,93 @@ void rec(jz_knn_index *ix, int i) {
   if (ix->timing) JZ_CUDA(cudaEventRecord(ix->ev[i], ix->st));
 }
 
-__global__ void k_zrow_flags(const int32_t *__restrict__ perm, int64_t n, int64_t nq, int32_t *__restrict__ f) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    f[i] = perm[i] < nq;
+// ---- point types: a point is a query iff its input position < n_query,
+// a source iff its gidx (.w) >= 0. After the joint sort + tree build the points are separated
+// into type-specific z-ordered arrays with per-type leaf splits.
+__global__ void k_type_flags(const float4 *__restrict__ pts, const int32_t *__restrict__ perm, int64_t n, int64_t nq,
+                             int32_t *__restrict__ fs, int32_t *__restrict__ fq) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    fs[i] = __float_as_int(pts[i].w) >= 0;
+    fq[i] = perm[i] < nq;
+  }
 }
-__global__ void k_i64_to_i32(const int64_t *__restrict__ a, int64_t n, int32_t *__restrict__ b) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    b[i] = (int32_t)a[i];
+__global__ void k_type_scatter(const float4 *__restrict__ pts, const int32_t *__restrict__ perm, int64_t n, int64_t nq,
+                               const int64_t *__restrict__ srank, const int64_t *__restrict__ qrank,
+                               float4 *__restrict__ spts, float4 *__restrict__ qpts, int32_t *__restrict__ qin) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    float4 p = pts[i];
+    const int in = perm[i];
+    const int g = __float_as_int(p.w);
+    if (spts && g >= 0) spts[srank[i]] = p;
+    if (qpts && in < nq) {
+      if (g < 0) p.w = __int_as_float(in);  // query-only point: report its input row
+      qpts[qrank[i]] = p;
+      qin[qrank[i]] = in;
+    }
+  }
+}
+__global__ void k_type_beg(const int32_t *__restrict__ beg, int64_t m, const int64_t *__restrict__ srank,
+                           const int64_t *__restrict__ qrank, int32_t *__restrict__ sbeg, int32_t *__restrict__ qbeg) {
+  for (int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; l < m; l += (int64_t)gridDim.x * blockDim.x) {
+    if (sbeg) sbeg[l] = (int32_t)srank[beg[l]];
+    if (qbeg) qbeg[l] = (int32_t)qrank[beg[l]];
+  }
+}
+__global__ void k_pack_xq(const float *__restrict__ qry, int64_t nq, const float *__restrict__ src, int64_t ns,
+                          float4 *__restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nq + ns; i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < nq) out[i] = make_float4(qry[3 * i], qry[3 * i + 1], qry[3 * i + 2], __int_as_float(-1));
+    else {
+      const int64_t j = i - nq;
+      out[i] = make_float4(src[3 * j], src[3 * j + 1], src[3 * j + 2], __int_as_float((int)j));
+    }
+  }
+}
+
+void split_types(jz_knn_index *ix, bool typed) {
+  const int64_t n = ix->n, nleaf = ix->planes[0].nnodes;
+  cudaStream_t st = ix->st;
+  ix->spts = ix->qpts = ix->pts;
+  ix->sbeg = ix->qbeg = ix->planes[0].beg;
+  ix->qin = ix->perm;
+  ix->n_src = n;
+  if (!typed) return;
+  int32_t *fs = nullptr, *fq = nullptr;
+  int64_t *sr = nullptr, *qr = nullptr;
+  JZ_CUDA(cudaMallocAsync(&fs, n * sizeof(int32_t), st));
+  JZ_CUDA(cudaMallocAsync(&fq, n * sizeof(int32_t), st));
+  JZ_CUDA(cudaMallocAsync(&sr, (n + 1) * sizeof(int64_t), st));
+  JZ_CUDA(cudaMallocAsync(&qr, (n + 1) * sizeof(int64_t), st));
+  k_type_flags<<<jz::grid_for(n, 256), 256, 0, st>>>(ix->pts, ix->perm, n, ix->n_query, fs, fq);
+  JZ_LAUNCH_CHECK();
+  jz::exclusive_scan_i32_to_i64(fs, sr, n, st);
+  jz::exclusive_scan_i32_to_i64(fq, qr, n, st);
+  ix->n_src = jz::read_i64(sr + n, st);
+  const bool sep_s = ix->n_src < n, sep_q = ix->n_query < n;
+  if (sep_s) {
+    JZ_CUDA(cudaMallocAsync(&ix->spts, (ix->n_src > 0 ? ix->n_src : 1) * sizeof(float4), st));
+    JZ_CUDA(cudaMallocAsync(&ix->sbeg, (nleaf + 1) * sizeof(int32_t), st));
+    ix->own_s = true;
+  }
+  if (sep_q || sep_s) {  // query-only points get their input row in .w
+    JZ_CUDA(cudaMallocAsync(&ix->qpts, (ix->n_query > 0 ? ix->n_query : 1) * sizeof(float4), st));
+    JZ_CUDA(cudaMallocAsync(&ix->qbeg, (nleaf + 1) * sizeof(int32_t), st));
+    JZ_CUDA(cudaMallocAsync(&ix->qin, (ix->n_query > 0 ? ix->n_query : 1) * sizeof(int32_t), st));
+    ix->own_q = true;
+  }
+  if (sep_s || sep_q) {
+    k_type_scatter<<<jz::grid_for(n, 256), 256, 0, st>>>(ix->pts, ix->perm, n, ix->n_query, sr, qr,
+                                                         sep_s ? ix->spts : nullptr, ix->own_q ? ix->qpts : nullptr,
+                                                         ix->own_q ? ix->qin : nullptr);
+    JZ_LAUNCH_CHECK();
+    k_type_beg<<<jz::grid_for(nleaf + 1, 256), 256, 0, st>>>(ix->planes[0].beg, nleaf + 1, sr, qr,
+                                                             sep_s ? ix->sbeg : nullptr, ix->own_q ? ix->qbeg : nullptr);
+    JZ_LAUNCH_CHECK();
+  }
+  JZ_CUDA(cudaFreeAsync(fs, st));
+  JZ_CUDA(cudaFreeAsync(fq, st));
+  JZ_CUDA(cudaFreeAsync(sr, st));
+  JZ_CUDA(cudaFreeAsync(qr, st));
 }
 
 jz_knn_index *build_impl(const float *pos, int64_t n, int stride, int gidx_mode, int64_t n_query, const float *box,
@@ -145,20 +228,7 @@ jz_knn_index *build_impl(const float *pos, int64_t n, int stride, int gidx_mode,
     jz::sort_points(pos, n, stride, gidx_mode, 0, frame, ix->keys, ix->perm, ix->pts, st);
     rec(ix, 2);
     jz::build_planes(ix->keys, ix->pts, n, prm, ix->planes, st);
-    if (n_query < n) {  // z-order row of each query (ghost-carrying builds)
-      int32_t *f = nullptr;
-      int64_t *ps = nullptr;
-      JZ_CUDA(cudaMallocAsync(&f, n * sizeof(int32_t), st));
-      JZ_CUDA(cudaMallocAsync(&ps, (n + 1) * sizeof(int64_t), st));
-      JZ_CUDA(cudaMallocAsync(&ix->zrow, n * sizeof(int32_t), st));
-      k_zrow_flags<<<jz::grid_for(n, 256), 256, 0, st>>>(ix->perm, n, n_query, f);
-      JZ_LAUNCH_CHECK();
-      jz::exclusive_scan_i32_to_i64(f, ps, n, st);
-      k_i64_to_i32<<<jz::grid_for(n, 256), 256, 0, st>>>(ps, n, ix->zrow);
-      JZ_LAUNCH_CHECK();
-      JZ_CUDA(cudaFreeAsync(f, st));
-      JZ_CUDA(cudaFreeAsync(ps, st));
-    }
+    split_types(ix, gidx_mode != 0);
     rec(ix, 3);
     if (ix->timing) {
       JZ_CUDA(cudaEventSynchronize(ix->ev[3]));
@@ -212,6 +282,29 @@ int jz_knn_build_xyzg(const float *pts4, int64_t n, int64_t n_query, const float
   JZ_API_END
 }
 
+int jz_knn_build_xq(const float *src, int64_t n_src, const float *qry, int64_t n_qry, const float *box,
+                    const jz_knn_params *p, jz_stream_t s, jz_knn_index **out) {
+  JZ_API_BEGIN
+  if (!out || !src || (!qry && n_qry > 0)) return fail(JZ_EINVAL, "NULL argument");
+  if (n_src < 1 || n_qry < 0 || n_src + n_qry > (int64_t)INT32_MAX - 1)
+    return fail(JZ_EINVAL, "need n_src >= 1, n_qry >= 0, n_src + n_qry <= 2^31 - 2");
+  cudaStream_t st = (cudaStream_t)s;
+  init_pool();
+  float4 *tmp = nullptr;
+  JZ_CUDA(cudaMallocAsync(&tmp, (n_src + n_qry) * sizeof(float4), st));
+  k_pack_xq<<<jz::grid_for(n_src + n_qry, 256), 256, 0, st>>>(qry, n_qry, src, n_src, tmp);
+  JZ_LAUNCH_CHECK();
+  try {
+    *out = build_impl(reinterpret_cast<const float *>(tmp), n_src + n_qry, 4, 1, n_qry, box, p, st);
+  } catch (...) {
+    cudaFreeAsync(tmp, st);
+    throw;
+  }
+  JZ_CUDA(cudaFreeAsync(tmp, st));
+  return JZ_OK;
+  JZ_API_END
+}
+
 int jz_knn_rows(const jz_knn_index *ix, int64_t *m) {
   if (!ix || !m) return fail(JZ_EINVAL, "NULL argument");
   *m = ix->n_query;
@@ -221,11 +314,12 @@ int jz_knn_rows(const jz_knn_index *ix, int64_t *m) {
 int jz_knn_query(jz_knn_index *ix, int k, int order, int32_t *out_idx, float *out_d2, int32_t *out_row_gidx,
                  jz_stream_t s) {
   JZ_API_BEGIN
-  if (!ix || !out_idx || !out_d2) return fail(JZ_EINVAL, "NULL argument");
-  if (k < 1 || k > jz::kMaxK) return fail(JZ_EINVAL, "k must be in [1, 32]");
-  if (k > ix->n) return fail(JZ_EINVAL, "k must not exceed the number of points");
+  if (!ix) return fail(JZ_EINVAL, "NULL index");
+  if (ix->n_query > 0 && (!out_idx || !out_d2)) return fail(JZ_EINVAL, "NULL argument");
+  if (k < 1) return fail(JZ_EINVAL, "k must be >= 1");
+  if (k > ix->n_src) return fail(JZ_EINVAL, "k must not exceed the number of source points");
   if (order != JZ_ORDER_INPUT && order != JZ_ORDER_Z) return fail(JZ_EINVAL, "bad order");
-  if (order == JZ_ORDER_Z && !out_row_gidx) return fail(JZ_EINVAL, "JZ_ORDER_Z needs out_row_gidx");
+  if (order == JZ_ORDER_Z && !out_row_gidx && ix->n_query > 0) return fail(JZ_EINVAL, "JZ_ORDER_Z needs out_row_gidx");
   cudaStream_t st = (cudaStream_t)s;
   ix->st = st;
   if (ix->n_query == 0) return JZ_OK;
@@ -240,17 +334,17 @@ int jz_knn_query(jz_knn_index *ix, int k, int order, int32_t *out_idx, float *ou
   JZ_CUDA(cudaMemsetAsync(ix->d_evals, 0, 16 * sizeof(unsigned long long), st));
   const bool one_plane = ix->planes.size() == 1;
   jz::LeafArgs la;
-  la.pts = ix->pts;
-  la.leaf_beg = ix->planes[0].beg;
+  la.spts = ix->spts;
+  la.sbeg = ix->sbeg;
+  la.qpts = ix->qpts;
+  la.qbeg = ix->qbeg;
+  la.qin = ix->qin;
   la.leaf_box = ix->planes[0].box;
   la.par_leaf = one_plane ? superbeg : ix->planes[1].beg;
   la.par_box = one_plane ? nullptr : ix->planes[1].box;
   la.npar = il.nrecv;
   la.il = &il;
   la.rmax2 = rmax2;
-  la.perm = ix->perm;
-  la.zrow = ix->zrow;
-  la.n_query = ix->n_query;
   la.k = k;
   la.order = order;
   la.flags = ix->prm.flags;
@@ -282,11 +376,19 @@ int jz_knn_query(jz_knn_index *ix, int k, int order, int32_t *out_idx, float *ou
 void jz_knn_free(jz_knn_index *ix) {
   if (!ix) return;
   cudaStream_t st = ix->st;
+  if (ix->own_s) {
+    cudaFreeAsync(ix->spts, st);
+    cudaFreeAsync(ix->sbeg, st);
+  }
+  if (ix->own_q) {
+    cudaFreeAsync(ix->qpts, st);
+    cudaFreeAsync(ix->qbeg, st);
+    cudaFreeAsync(ix->qin, st);
+  }
   jz::free_planes(ix->planes, st);
   if (ix->pts) cudaFreeAsync(ix->pts, st);
   if (ix->keys) cudaFreeAsync(ix->keys, st);
   if (ix->perm) cudaFreeAsync(ix->perm, st);
-  if (ix->zrow) cudaFreeAsync(ix->zrow, st);
   if (ix->d_evals) cudaFreeAsync(ix->d_evals, st);
   cudaStreamSynchronize(st);
   for (auto &e : ix->ev)
@@ -299,7 +401,7 @@ int jz_knn_search_host(const float *pos_host, int64_t n, const float *box, const
   JZ_API_BEGIN
   if (!pos_host || !idx_host || !d2_host) return fail(JZ_EINVAL, "NULL argument");
   if (n < 1) return fail(JZ_EINVAL, "n must be >= 1");
-  if (k < 1 || k > jz::kMaxK || k > n) return fail(JZ_EINVAL, "k must be in [1, min(32, n)]");
+  if (k < 1 || k > n) return fail(JZ_EINVAL, "k must be in [1, n]");
   cudaStream_t st = (cudaStream_t)s;
   init_pool();
   float *dpos = nullptr;

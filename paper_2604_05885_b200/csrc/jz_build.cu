@@ -143,7 +143,8 @@ __global__ void k_iota(int32_t *__restrict__ a, int64_t m) {
     a[j] = (int32_t)j;
 }
 
-// one warp per leaf: AABB of its points + count
+// one warp per leaf: AABB of its points (all types) + number of SOURCE points (gidx >= 0):
+// the count heap of FindRmax counts neighbour candidates (P:L276-279 joint tree over types)
 __global__ void k_leaf_boxes(const float4 *__restrict__ pts, const int32_t *__restrict__ beg, int64_t nleaf,
                              NodeBox *__restrict__ box) {
   const int lane = threadIdx.x & 31;
@@ -152,8 +153,10 @@ __global__ void k_leaf_boxes(const float4 *__restrict__ pts, const int32_t *__re
   for (; w < nleaf; w += nw) {
     const int b = beg[w], e = beg[w + 1];
     float lx = INFINITY, ly = INFINITY, lz = INFINITY, hx = -INFINITY, hy = -INFINITY, hz = -INFINITY;
+    int ns = 0;
     for (int i = b + lane; i < e; i += 32) {
       float4 p = pts[i];
+      ns += __float_as_int(p.w) >= 0;
       lx = fminf(lx, p.x);
       ly = fminf(ly, p.y);
       lz = fminf(lz, p.z);
@@ -169,10 +172,11 @@ __global__ void k_leaf_boxes(const float4 *__restrict__ pts, const int32_t *__re
       hx = fmaxf(hx, __shfl_xor_sync(0xffffffffu, hx, o));
       hy = fmaxf(hy, __shfl_xor_sync(0xffffffffu, hy, o));
       hz = fmaxf(hz, __shfl_xor_sync(0xffffffffu, hz, o));
+      ns += __shfl_xor_sync(0xffffffffu, ns, o);
     }
     if (lane == 0) {
       NodeBox nb;
-      nb.lo = make_float4(lx, ly, lz, __int_as_float(e - b));
+      nb.lo = make_float4(lx, ly, lz, __int_as_float(ns));
       nb.hi = make_float4(hx, hy, hz, 0.f);
       box[w] = nb;
     }

@@ -240,7 +240,7 @@ int jz_knn_plane_nodes(const jz_knn_index *ix, int plane, int64_t *nnodes) {
 }
 
 int jz_knn_query_boxes(jz_knn_index *ix, int k, int plane, int rank, float *boxes, jz_stream_t s) {
-  if (!ix || !boxes || k < 1 || k > jz::kMaxK) return JZ_EINVAL;
+  if (!ix || !boxes || k < 1) return JZ_EINVAL;
   try {
     cudaStream_t st = (cudaStream_t)s;
     jz::IndexView v = jz::view_of(ix);

@@ -58,18 +58,18 @@ void walk_to(const std::vector<Plane> &planes, const Dom &D, int k, int ngr, uns
 
 // leaf-to-leaf (jz_leaf.cu)
 struct LeafArgs {
-  const float4 *pts;
-  const int32_t *leaf_beg;  // [nleaf+1]
+  const float4 *spts;       // source points (z order)
+  const int32_t *sbeg;      // [nleaf+1] first source of each leaf
+  const float4 *qpts;       // query points (z order); .w = gidx, or the input row of a query-only point
+  const int32_t *qbeg;      // [nleaf+1] first query of each leaf
+  const int32_t *qin;       // [nq] input row of each query
   const NodeBox *leaf_box;  // [nleaf]
   const int32_t *par_leaf;  // [npar+1] first leaf of each receiving parent
   const NodeBox *par_box;   // [npar] or nullptr
   int64_t npar;
   const IList *il;          // receivers = parents
   const float *rmax2;       // [npar] or nullptr
-  const int32_t *perm;      // sorted position -> input position
-  const int32_t *zrow;      // sorted position -> z-order query row (nullptr: identity)
-  int64_t n_query;          // input positions < n_query are queries
-  int k;
+  int k;                    // any k >= 1: ceil(k / kMaxK) kernel passes
   int order;
   unsigned flags;
   int32_t *out_idx;

@@ -80,8 +80,11 @@ __device__ __forceinline__ void topk_insert(u64 (&a)[K], u64 key) {
 }
 
 struct LeafPK {
-  const float4 *pts;
-  const int32_t *leaf_beg;   // [nleaf+1] first point of each leaf
+  const float4 *spts;        // source points, z order (type-separated)
+  const int32_t *sbeg;       // [nleaf+1] first source of each leaf
+  const float4 *qpts;        // query points, z order
+  const int32_t *qbeg;       // [nleaf+1] first query of each leaf
+  const int32_t *qin;        // [nq] input row of each query
   const NodeBox *leaf_box;   // [nleaf]
   const int32_t *par_leaf;   // [npar+1] first leaf of each receiving parent
   const NodeBox *par_box;    // [npar] or nullptr
@@ -92,10 +95,9 @@ struct LeafPK {
   const int32_t *item_par;   // [nitems] receiving parent of each 32-query work item
   const int32_t *item_q0;    // [nitems] first query (sorted position) of the item
   int64_t nitems;
-  const int32_t *perm;
-  const int32_t *zrow;
-  int64_t n_query;
-  int k;
+  int k;      // neighbours found by this pass (<= K)
+  int col0;   // first output column of this pass (k > k_max chunking)
+  int ldo;    // output row stride (total k)
   int order;
   int early;
   int sorted;
@@ -103,7 +105,6 @@ struct LeafPK {
   float *out_d2;
   int32_t *out_row_gidx;
   unsigned long long *stats;  // [0] distance evaluations, [1] top-k insertions (or nullptr)
-  const float *seed_d2;       // diagnostics only: per-row k-th d2 of a previous run (or nullptr)
 };
 
 // per-axis shift class of a (query box, source box) pair: 0 = no wrap for any pair,
@@ -134,9 +135,10 @@ struct WarpBuf {
   u64 q[kQCap][32];  // candidate queue, lane-minor
 };
 
-template <int K>
+template <int K, bool LB>
 struct Lane {
   u64 tk[K];
+  u64 lb;    // keys <= lb were found by earlier passes (0 on the first pass)
   float kth;
   unsigned ins;
   int qn;    // queued candidates
@@ -145,8 +147,8 @@ struct Lane {
 
 // Insert the lane's queued candidates: all lanes drain their queues in parallel, so the
 // warp runs max(queue length) insertion rounds instead of one per candidate group.
-template <int K>
-__device__ __forceinline__ void flush(WarpBuf &B, Lane<K> &L) {
+template <int K, bool LB>
+__device__ __forceinline__ void flush(WarpBuf &B, Lane<K, LB> &L) {
   const int lane = threadIdx.x & 31;
   const int mx = __reduce_max_sync(0xffffffffu, (unsigned)L.qn);
   for (int i = 0; i < mx; ++i) {
@@ -162,11 +164,11 @@ __device__ __forceinline__ void flush(WarpBuf &B, Lane<K> &L) {
   L.qn = 0;
 }
 
-template <int K>
-__device__ __forceinline__ void cand(Lane<K> &L, float d2, int g) {
+template <int K, bool LB>
+__device__ __forceinline__ void cand(Lane<K, LB> &L, float d2, int g) {
   if (d2 <= L.kth) {
     const u64 key = ((u64)__float_as_uint(d2) << 32) | (unsigned)(g + 1);
-    if (key < L.tk[K - 1]) {
+    if (key < L.tk[K - 1] && (!LB || key > L.lb)) {
       topk_insert<K>(L.tk, key);
       L.kth = __uint_as_float((unsigned)(L.tk[K - 1] >> 32));
       ++L.ins;
@@ -174,18 +176,21 @@ __device__ __forceinline__ void cand(Lane<K> &L, float d2, int g) {
   }
 }
 
-template <int K>
-__device__ __forceinline__ void enqueue(WarpBuf &B, Lane<K> &L, float d2, int g) {
+template <int K, bool LB>
+__device__ __forceinline__ void enqueue(WarpBuf &B, Lane<K, LB> &L, float d2, int g) {
   if (d2 <= L.kth) {
-    B.q[L.qn][threadIdx.x & 31] = ((u64)__float_as_uint(d2) << 32) | (unsigned)(g + 1);
-    ++L.qn;
+    const u64 key = ((u64)__float_as_uint(d2) << 32) | (unsigned)(g + 1);
+    if (!LB || key > L.lb) {
+      B.q[L.qn][threadIdx.x & 31] = key;
+      ++L.qn;
+    }
   }
 }
 
 // evaluate staged sources [0, n) (n multiple of 4, NaN padded) against the lane's query
-template <int K, bool SHIFT>
+template <int K, bool LB, bool SHIFT>
 __device__ __forceinline__ void eval_block(WarpBuf &B, int n, float qx, float qy, float qz, float shx, float shy,
-                                           float shz, Lane<K> &L) {
+                                           float shz, Lane<K, LB> &L) {
   const u64 QX = pk(qx, qx), QY = pk(qy, qy), QZ = pk(qz, qz);
   const u64 SX = pk(shx, shx), SY = pk(shy, shy), SZ = pk(shz, shz);
   for (int j = 0; j < n; j += 4) {
@@ -211,22 +216,22 @@ __device__ __forceinline__ void eval_block(WarpBuf &B, int n, float qx, float qy
     const float m = fminf(fminf(a0, a1), fminf(a2, a3));  // NaN padding is ignored by min
     if (__any_sync(0xffffffffu, m <= L.kth)) {
       const int4 G = *reinterpret_cast<const int4 *>(&B.g[j]);
-      enqueue<K>(B, L, a0, G.x);
-      enqueue<K>(B, L, a1, G.y);
-      enqueue<K>(B, L, a2, G.z);
-      enqueue<K>(B, L, a3, G.w);
-      if (__any_sync(0xffffffffu, L.qn > kQCap - 4)) flush<K>(B, L);
+      enqueue<K, LB>(B, L, a0, G.x);
+      enqueue<K, LB>(B, L, a1, G.y);
+      enqueue<K, LB>(B, L, a2, G.z);
+      enqueue<K, LB>(B, L, a3, G.w);
+      if (__any_sync(0xffffffffu, L.qn > kQCap - 4)) flush<K, LB>(B, L);
     }
   }
-  if (__any_sync(0xffffffffu, L.qn > 0)) flush<K>(B, L);
+  if (__any_sync(0xffffffffu, L.qn > 0)) flush<K, LB>(B, L);
 }
 
-template <int K>
+template <int K, bool LB>
 __device__ __forceinline__ void eval_generic(const WarpBuf &B, int n, float qx, float qy, float qz, const Dom &D,
-                                             Lane<K> &L) {
+                                             Lane<K, LB> &L) {
   for (int j = 0; j < n; ++j) {
     const float d2 = canon_d2_per(qx, qy, qz, B.x[j], B.y[j], B.z[j], D);  // NaN padding -> NaN
-    cand<K>(L, d2, B.g[j]);
+    cand<K, LB>(L, d2, B.g[j]);
   }
 }
 
@@ -234,10 +239,10 @@ __device__ __forceinline__ void eval_generic(const WarpBuf &B, int n, float qx, 
 // leaf (exact box bound vs the warp's current max k-th distance), then every lane tests its own
 // query against each surviving leaf (skip unless some lane needs it); survivors are staged in
 // batches of one periodic shift class and evaluated.
-template <int K, bool PER>
+template <int K, bool LB, bool PER>
 __device__ __forceinline__ void visit_leaves(const LeafPK &a, const Dom &D, WarpBuf &B, const NodeBox &wbox, float wmax,
                                              int la, int lb, int xa, int xb, float qx, float qy, float qz, bool act,
-                                             Lane<K> &L, unsigned long long &nev) {
+                                             Lane<K, LB> &L, unsigned long long &nev) {
   const int lane = threadIdx.x & 31;
   for (int l0 = la; l0 < lb; l0 += 32) {
     const int l = l0 + lane;
@@ -271,13 +276,13 @@ __device__ __forceinline__ void visit_leaves(const LeafPK &a, const Dom &D, Warp
             continue;
           }
         }
-        const int lp = a.leaf_beg[l0 + src], m = a.leaf_beg[l0 + src + 1] - lp;
+        const int lp = a.sbeg[l0 + src], m = a.sbeg[l0 + src + 1] - lp;
         if (n + ((m + 3) & ~3) > kLCap) break;
         bal &= bal - 1;
         for (int t = lane; t < ((m + 3) & ~3); t += 32) {
           float4 p = make_float4(__int_as_float(0x7fc00000), __int_as_float(0x7fc00000), __int_as_float(0x7fc00000),
                                  0.f);
-          if (t < m) p = a.pts[lp + t];
+          if (t < m) p = a.spts[lp + t];
           B.x[n + t] = p.x;
           B.y[n + t] = p.y;
           B.z[n + t] = p.z;
@@ -289,16 +294,16 @@ __device__ __forceinline__ void visit_leaves(const LeafPK &a, const Dom &D, Warp
       __syncwarp();
       if (n == 0) continue;
       if (!PER || c0 == 0) {
-        eval_block<K, false>(B, n, qx, qy, qz, 0.f, 0.f, 0.f, L);
+        eval_block<K, LB, false>(B, n, qx, qy, qz, 0.f, 0.f, 0.f, L);
       } else if (!any_straddle(c0)) {  // no axis straddles: uniform exact shift
         float s0, s1, s2;
         const NodeBox lbx = a.leaf_box[l0 + first];
         shift_class(wbox.lo.x, wbox.hi.x, lbx.lo.x, lbx.hi.x, D.L[0], D.h[0], s0);
         shift_class(wbox.lo.y, wbox.hi.y, lbx.lo.y, lbx.hi.y, D.L[1], D.h[1], s1);
         shift_class(wbox.lo.z, wbox.hi.z, lbx.lo.z, lbx.hi.z, D.L[2], D.h[2], s2);
-        eval_block<K, true>(B, n, qx, qy, qz, s0, s1, s2, L);
+        eval_block<K, LB, true>(B, n, qx, qy, qz, s0, s1, s2, L);
       } else {
-        eval_generic<K>(B, n, qx, qy, qz, D, L);
+        eval_generic<K, LB>(B, n, qx, qy, qz, D, L);
       }
       __syncwarp();
     }
@@ -309,7 +314,7 @@ __device__ __forceinline__ float warp_max_kth(float kth) {
   return __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(fmaxf(kth, 0.f))));
 }
 
-template <int K, bool PER>
+template <int K, bool LB, bool PER>
 __global__ void __launch_bounds__(kLThreads) k_leaf(LeafPK a, Dom D) {
   __shared__ __align__(16) WarpBuf s_buf[kLWarps];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -318,21 +323,19 @@ __global__ void __launch_bounds__(kLThreads) k_leaf(LeafPK a, Dom D) {
   WarpBuf &B = s_buf[warp];
   const int J = a.item_par[item];
   const int LJa = a.par_leaf[J], LJb = a.par_leaf[J + 1];
-  const int qhi = a.leaf_beg[LJb];
+  const int qhi = a.qbeg[LJb];
   const int q0 = a.item_q0[item];
   const int qi = q0 + lane;
-  bool act = qi < qhi;
+  const bool act = qi < qhi;
   float qx = 0.f, qy = 0.f, qz = 0.f, qw = 0.f;
-  int inpos = 0;
   if (act) {
-    const float4 q = a.pts[qi];
+    const float4 q = a.qpts[qi];
     qx = q.x;
     qy = q.y;
     qz = q.z;
     qw = q.w;
-    inpos = a.perm[qi];
-    act = inpos < a.n_query;
   }
+  const int64_t row = !act ? 0 : (a.order == JZ_ORDER_INPUT ? (int64_t)a.qin[qi] : (int64_t)qi);
   if (!__any_sync(0xffffffffu, act)) return;
   float blo[3] = {act ? qx : INFINITY, act ? qy : INFINITY, act ? qz : INFINITY};
   float bhi[3] = {act ? qx : -INFINITY, act ? qy : -INFINITY, act ? qz : -INFINITY};
@@ -348,17 +351,18 @@ __global__ void __launch_bounds__(kLThreads) k_leaf(LeafPK a, Dom D) {
   wbox.lo = make_float4(blo[0], blo[1], blo[2], 0.f);
   wbox.hi = make_float4(bhi[0], bhi[1], bhi[2], 0.f);
 
-  float R0 = a.rmax2 ? a.rmax2[J] : INFINITY;
-  if (a.seed_d2 && act) {
-    const int64_t row = a.order == JZ_ORDER_INPUT ? (int64_t)inpos : (a.zrow ? (int64_t)a.zrow[qi] : (int64_t)qi);
-    R0 = a.seed_d2[row * a.k + a.k - 1];
-  }
-  Lane<K> L;
+  const float R0 = a.rmax2 ? a.rmax2[J] : INFINITY;
+  Lane<K, LB> L;
   {
     const u64 sentinel = ((u64)__float_as_uint(R0) << 32) | 0xffffffffull;
 #pragma unroll
     for (int j = 0; j < K; ++j) L.tk[j] = (j < K - a.k) ? 0ull : sentinel;
     L.kth = act ? R0 : -1.f;  // inactive lanes never pass a comparison
+    L.lb = 0;
+    if (LB && act) {  // continue after the last (d2, index) of the previous pass
+      const int64_t o = row * a.ldo + a.col0 - 1;
+      L.lb = ((u64)__float_as_uint(a.out_d2[o]) << 32) | (unsigned)(a.out_idx[o] + 1);
+    }
     L.ins = 0;
     L.qn = 0;
     L.act = act;
@@ -370,14 +374,14 @@ __global__ void __launch_bounds__(kLThreads) k_leaf(LeafPK a, Dom D) {
     const int qend = min(q0 + 32, qhi);
     for (int l0 = LJa; l0 < LJb; l0 += 32) {
       const int l = l0 + lane;
-      const bool ov = l < LJb && a.leaf_beg[l] < qend && a.leaf_beg[l + 1] > q0;
+      const bool ov = l < LJb && a.qbeg[l] < qend && a.qbeg[l + 1] > q0;
       const unsigned b = __ballot_sync(0xffffffffu, ov);
       if (b) {
         xa = min(xa, l0 + __ffs(b) - 1);
         xb = max(xb, l0 + 32 - __clz(b));
       }
     }
-    visit_leaves<K, PER>(a, D, B, wbox, INFINITY, xa, xb, 0, 0, qx, qy, qz, act, L, nev);
+    visit_leaves<K, LB, PER>(a, D, B, wbox, INFINITY, xa, xb, 0, 0, qx, qy, qz, act, L, nev);
   }
   const int64_t eb = a.ispl[J], ee = a.ispl[J + 1];
   for (int64_t e = eb; e < ee; ++e) {
@@ -388,7 +392,7 @@ __global__ void __launch_bounds__(kLThreads) k_leaf(LeafPK a, Dom D) {
       continue;
     }
     if (a.par_box && box_dlow2(wbox, a.par_box[S], D) > wmax) continue;
-    visit_leaves<K, PER>(a, D, B, wbox, wmax, a.par_leaf[S], a.par_leaf[S + 1], S == J ? xa : 0, S == J ? xb : 0, qx,
+    visit_leaves<K, LB, PER>(a, D, B, wbox, wmax, a.par_leaf[S], a.par_leaf[S + 1], S == J ? xa : 0, S == J ? xb : 0, qx,
                          qy, qz, act, L, nev);
   }
   if (a.stats) {
@@ -404,432 +408,8 @@ __global__ void __launch_bounds__(kLThreads) k_leaf(LeafPK a, Dom D) {
     }
   }
   if (act) {
-    const int64_t row = a.order == JZ_ORDER_INPUT ? (int64_t)inpos : (a.zrow ? (int64_t)a.zrow[qi] : (int64_t)qi);
-    int32_t *oi = a.out_idx + row * a.k;
-    float *od = a.out_d2 + row * a.k;
-#pragma unroll
-    for (int j = 0; j < K; ++j) {
-      if (j >= K - a.k) {
-        oi[j - (K - a.k)] = (int32_t)((unsigned)(L.tk[j] & 0xffffffffu) - 1u);
-        od[j - (K - a.k)] = __uint_as_float((unsigned)(L.tk[j] >> 32));
-      }
-    }
-    if (a.out_row_gidx) a.out_row_gidx[row] = __float_as_int(qw);
-  }
-}
-
-// =====================================================================================
-// Warp-specialised LeafToLeaf (experimental, JZ_FLAG_WS_LEAF; slower than k_leaf in round 1:
-// the single producer warp's dependent-load chain starves the consumers). One CTA per work item = up to 128 consecutive queries
-// of a receiving plane-1 node J: warp 0 is the producer, warps 1..4 are consumers (32 queries
-// each). The producer walks J's interaction list once for all 128 queries (J's own leaves
-// first, then the list in r_low order), prunes leaves with the exact box bound against the
-// CTA's query box and the consumers' published k-th bounds, and stages surviving leaves as
-// NaN-padded x/y/z/gidx arrays into a 3-slot shared-memory ring. Full/empty mbarriers hand
-// slots over: consumers never stall on the walk's dependent loads, and the walk and staging
-// are shared by four warps. Each consumer re-tests every staged leaf against its own query box
-// and lanes, evaluates survivors with the packed f32x2 loop and drains its candidate queue
-// once per slot.
-// =====================================================================================
-constexpr int kWC = 4;                 // consumer warps
-constexpr int kWThreads = (kWC + 1) * 32;
-constexpr int kRS = 3;                 // ring slots
-constexpr int kSCap = 256;             // staged points per slot
-constexpr int kSSeg = 32;              // leaves per slot
-
-struct Slot {
-  float x[kSCap], y[kSCap], z[kSCap];
-  int g[kSCap];
-  NodeBox box[kSSeg];
-  int off[kSSeg], len[kSSeg], leaf[kSSeg];
-  int nseg;  // -1 = end of stream
-};
-
-struct WSShared {
-  Slot ring[kRS];
-  Slot own[kWC];  // consumers' private slot for their own-leaf pre-pass
-  u64 q[kWC][kQCap][32];
-  unsigned long long full[kRS], empty[kRS];
-  float wmax[kWC];
-  NodeBox wbox[kWC];
-};
-
-__device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
-  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(unsigned long long *bar) {
-  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
-  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}" ::"r"(a) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity) {
-  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
-  asm volatile(
-      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(a),
-      "r"(parity)
-      : "memory");
-}
-
-template <int K>
-__device__ __forceinline__ void wflush(u64 (*q)[32], Lane<K> &L) {
-  const int lane = threadIdx.x & 31;
-  const int mx = __reduce_max_sync(0xffffffffu, (unsigned)L.qn);
-  for (int i = 0; i < mx; ++i) {
-    if (i < L.qn) {
-      const u64 key = q[i][lane];
-      if (key < L.tk[K - 1]) {
-        topk_insert<K>(L.tk, key);
-        ++L.ins;
-      }
-    }
-  }
-  L.kth = L.act ? __uint_as_float((unsigned)(L.tk[K - 1] >> 32)) : -1.f;
-  L.qn = 0;
-}
-
-template <int K>
-__device__ __forceinline__ void wenqueue(u64 (*q)[32], Lane<K> &L, float d2, int g) {
-  if (d2 <= L.kth) {
-    q[L.qn][threadIdx.x & 31] = ((u64)__float_as_uint(d2) << 32) | (unsigned)(g + 1);
-    ++L.qn;
-  }
-}
-
-// staged sources [j0, j0 + n) of a slot (n multiple of 4, NaN padded) against the lane's query
-template <int K, bool SHIFT>
-__device__ __forceinline__ void weval(const Slot &S, u64 (*q)[32], int j0, int n, float qx, float qy, float qz,
-                                      float shx, float shy, float shz, Lane<K> &L) {
-  const u64 QX = pk(qx, qx), QY = pk(qy, qy), QZ = pk(qz, qz);
-  const u64 SX = pk(shx, shx), SY = pk(shy, shy), SZ = pk(shz, shz);
-  for (int j = j0; j < j0 + n; j += 4) {
-    const float4 X = *reinterpret_cast<const float4 *>(&S.x[j]);
-    const float4 Y = *reinterpret_cast<const float4 *>(&S.y[j]);
-    const float4 Z = *reinterpret_cast<const float4 *>(&S.z[j]);
-    u64 tx0 = sub2(QX, pk(X.x, X.y)), tx1 = sub2(QX, pk(X.z, X.w));
-    u64 ty0 = sub2(QY, pk(Y.x, Y.y)), ty1 = sub2(QY, pk(Y.z, Y.w));
-    u64 tz0 = sub2(QZ, pk(Z.x, Z.y)), tz1 = sub2(QZ, pk(Z.z, Z.w));
-    if (SHIFT) {
-      tx0 = add2(tx0, SX);
-      tx1 = add2(tx1, SX);
-      ty0 = add2(ty0, SY);
-      ty1 = add2(ty1, SY);
-      tz0 = add2(tz0, SZ);
-      tz1 = add2(tz1, SZ);
-    }
-    const u64 d0 = fma2(tz0, tz0, fma2(ty0, ty0, mul2(tx0, tx0)));
-    const u64 d1 = fma2(tz1, tz1, fma2(ty1, ty1, mul2(tx1, tx1)));
-    float a0, a1, a2, a3;
-    upk(d0, a0, a1);
-    upk(d1, a2, a3);
-    const float m = fminf(fminf(a0, a1), fminf(a2, a3));
-    if (__any_sync(0xffffffffu, m <= L.kth)) {
-      if (__any_sync(0xffffffffu, L.qn > kQCap - 4)) wflush<K>(q, L);  // room for 4
-      const int4 G = *reinterpret_cast<const int4 *>(&S.g[j]);
-      wenqueue<K>(q, L, a0, G.x);
-      wenqueue<K>(q, L, a1, G.y);
-      wenqueue<K>(q, L, a2, G.z);
-      wenqueue<K>(q, L, a3, G.w);
-    }
-  }
-}
-
-template <int K>
-__device__ __forceinline__ void weval_generic(const Slot &S, u64 (*q)[32], int j0, int n, float qx, float qy,
-                                              float qz, const Dom &D, Lane<K> &L) {
-  for (int j = j0; j < j0 + n; ++j) {
-    const float d2 = canon_d2_per(qx, qy, qz, S.x[j], S.y[j], S.z[j], D);  // NaN padding -> NaN
-    if (__any_sync(0xffffffffu, L.qn >= kQCap)) wflush<K>(q, L);       // room for 1
-    wenqueue<K>(q, L, d2, S.g[j]);
-  }
-}
-
-template <int K, bool PER>
-__device__ __forceinline__ void wslot(const LeafPK &a, const Dom &D, const Slot &S, int ns, int xa, int xb,
-                                      const NodeBox &wbox, float qx, float qy, float qz, bool act, u64 (*q)[32],
-                                      Lane<K> &L, unsigned long long &nev) {
-  for (int s = 0; s < ns; ++s) {
-    const int lf = S.leaf[s];
-    if (lf >= xa && lf < xb) continue;  // evaluated in the pre-pass
-    const NodeBox bx = S.box[s];
-    const float wm = a.early ? warp_max_kth(L.kth) : INFINITY;
-    if (box_dlow2(wbox, bx, D) > wm) continue;
-    if (!__any_sync(0xffffffffu, act && pt_box_dlow2(qx, qy, qz, bx, D) <= L.kth)) continue;
-    const int off = S.off[s], m = S.len[s], mp = (m + 3) & ~3;
-    nev += act ? (unsigned)m : 0u;
-    int cls = 0;
-    float s0 = 0.f, s1 = 0.f, s2 = 0.f;
-    if (PER) {
-      cls = shift_class(wbox.lo.x, wbox.hi.x, bx.lo.x, bx.hi.x, D.L[0], D.h[0], s0);
-      cls |= shift_class(wbox.lo.y, wbox.hi.y, bx.lo.y, bx.hi.y, D.L[1], D.h[1], s1) << 2;
-      cls |= shift_class(wbox.lo.z, wbox.hi.z, bx.lo.z, bx.hi.z, D.L[2], D.h[2], s2) << 4;
-    }
-    if (!PER || cls == 0) weval<K, false>(S, q, off, mp, qx, qy, qz, 0.f, 0.f, 0.f, L);
-    else if (!any_straddle(cls)) weval<K, true>(S, q, off, mp, qx, qy, qz, s0, s1, s2, L);
-    else weval_generic<K>(S, q, off, mp, qx, qy, qz, D, L);
-  }
-  if (__any_sync(0xffffffffu, L.qn > 0)) wflush<K>(q, L);
-}
-
-struct ItemWS {
-  const int32_t *item_par;
-  const int32_t *item_q0;
-  int64_t nitems;
-};
-
-template <int K, bool PER>
-__global__ void __launch_bounds__(kWThreads) k_leafws(LeafPK a, ItemWS it, Dom D) {
-  extern __shared__ __align__(16) unsigned char s_raw[];
-  WSShared &W = *reinterpret_cast<WSShared *>(s_raw);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t item = blockIdx.x;
-  const int J = it.item_par[item];
-  const int LJa = a.par_leaf[J], LJb = a.par_leaf[J + 1];
-  const int qhi = a.leaf_beg[LJb];
-  const int q0 = it.item_q0[item];
-  const float R0 = a.rmax2 ? a.rmax2[J] : INFINITY;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kRS; ++s) {
-      mbar_init(&W.full[s], 1);
-      mbar_init(&W.empty[s], kWC);
-    }
-  }
-  // ---- consumer setup
-  const int cw = warp - 1;
-  const int qi = q0 + cw * 32 + lane;
-  bool act = false;
-  float qx = 0.f, qy = 0.f, qz = 0.f, qw = 0.f;
-  int inpos = 0;
-  Lane<K> L;
-  NodeBox wbox;
-  bool wact = false;
-  if (warp > 0) {
-    act = qi < qhi && cw * 32 < 128;
-    if (act) {
-      const float4 qq = a.pts[qi];
-      qx = qq.x;
-      qy = qq.y;
-      qz = qq.z;
-      qw = qq.w;
-      inpos = a.perm[qi];
-      act = inpos < a.n_query;
-    }
-    wact = __any_sync(0xffffffffu, act);
-    float blo[3] = {act ? qx : INFINITY, act ? qy : INFINITY, act ? qz : INFINITY};
-    float bhi[3] = {act ? qx : -INFINITY, act ? qy : -INFINITY, act ? qz : -INFINITY};
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        blo[d] = fminf(blo[d], __shfl_xor_sync(0xffffffffu, blo[d], o));
-        bhi[d] = fmaxf(bhi[d], __shfl_xor_sync(0xffffffffu, bhi[d], o));
-      }
-    }
-    wbox.lo = make_float4(blo[0], blo[1], blo[2], 0.f);
-    wbox.hi = make_float4(bhi[0], bhi[1], bhi[2], 0.f);
-    const u64 sentinel = ((u64)__float_as_uint(R0) << 32) | 0xffffffffull;
-#pragma unroll
-    for (int j = 0; j < K; ++j) L.tk[j] = (j < K - a.k) ? 0ull : sentinel;
-    L.kth = act ? R0 : -1.f;
-    L.ins = 0;
-    L.qn = 0;
-    L.act = act;
-    if (lane == 0) {
-      W.wbox[cw] = wbox;
-      W.wmax[cw] = wact ? R0 : -1.f;
-    }
-  }
-  __syncthreads();
-
-  if (warp == 0) {
-    // ================= producer =================
-    NodeBox cb;
-    cb.lo = make_float4(INFINITY, INFINITY, INFINITY, 0.f);
-    cb.hi = make_float4(-INFINITY, -INFINITY, -INFINITY, 0.f);
-#pragma unroll
-    for (int w = 0; w < kWC; ++w) {
-      if (W.wmax[w] >= 0.f) {
-        cb.lo.x = fminf(cb.lo.x, W.wbox[w].lo.x);
-        cb.lo.y = fminf(cb.lo.y, W.wbox[w].lo.y);
-        cb.lo.z = fminf(cb.lo.z, W.wbox[w].lo.z);
-        cb.hi.x = fmaxf(cb.hi.x, W.wbox[w].hi.x);
-        cb.hi.y = fmaxf(cb.hi.y, W.wbox[w].hi.y);
-        cb.hi.z = fmaxf(cb.hi.z, W.wbox[w].hi.z);
-      }
-    }
-    int itn = 0, n = 0, ns = 0;
-    Slot *S = &W.ring[0];
-    mbar_wait(&W.empty[0], 1);
-    auto bound = [&]() {
-      if (!a.early) return INFINITY;
-      float m = -1.f;
-#pragma unroll
-      for (int w = 0; w < kWC; ++w) m = fmaxf(m, ((volatile float *)W.wmax)[w]);
-      return m;
-    };
-    auto commit = [&](int nseg) {
-      __syncwarp();
-      if (lane == 0) {
-        S->nseg = nseg;
-        mbar_arrive(&W.full[itn % kRS]);
-      }
-      ++itn;
-      S = &W.ring[itn % kRS];
-      mbar_wait(&W.empty[itn % kRS], ((itn / kRS) & 1) ^ 1);
-      n = 0;
-      ns = 0;
-    };
-    const int64_t eb = a.ispl[J], ee = a.ispl[J + 1];
-    // own node J first (its leaves hold the queries), then the list in r_low order
-    for (int64_t e = eb - 1; e < ee; ++e) {
-      int Sx = J;
-      float wm = bound();
-      if (e >= eb) {
-        Sx = a.isrc[e];
-        if (Sx == J) continue;
-        if (a.rlow[e] > wm) {
-          if (a.sorted) break;
-          continue;
-        }
-        if (a.par_box && box_dlow2(cb, a.par_box[Sx], D) > wm) continue;
-      }
-      const int la = a.par_leaf[Sx], lb = a.par_leaf[Sx + 1];
-      for (int l0 = la; l0 < lb; l0 += 32) {
-        // lane-parallel: box test, leaf range and box of one leaf per lane (independent loads)
-        const int l = l0 + lane;
-        bool pass = false;
-        NodeBox lbx;
-        int lp0 = 0, lp1 = 0;
-        if (l < lb) {
-          lbx = a.leaf_box[l];
-          lp0 = a.leaf_beg[l];
-          lp1 = a.leaf_beg[l + 1];
-          pass = e < eb || box_dlow2(cb, lbx, D) <= wm;
-        }
-        unsigned bal = __ballot_sync(0xffffffffu, pass);
-        while (bal) {
-          const int src = __ffs(bal) - 1;
-          bal &= bal - 1;
-          const int lf = l0 + src;
-          const int lp = __shfl_sync(0xffffffffu, lp0, src);
-          const int m = __shfl_sync(0xffffffffu, lp1, src) - lp, mp = (m + 3) & ~3;
-          if (n + mp > kSCap || ns == kSSeg) commit(ns);
-          // all loads of the leaf first (up to 4 per lane), then the stores
-          float4 pv[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int t = lane + 32 * u;
-            pv[u] = make_float4(__int_as_float(0x7fc00000), __int_as_float(0x7fc00000), __int_as_float(0x7fc00000),
-                                0.f);
-            if (t < m) pv[u] = a.pts[lp + t];
-          }
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int t = lane + 32 * u;
-            if (t < mp) {
-              S->x[n + t] = pv[u].x;
-              S->y[n + t] = pv[u].y;
-              S->z[n + t] = pv[u].z;
-              S->g[n + t] = __float_as_int(pv[u].w);
-            }
-          }
-          if (lane == src) {
-            S->box[ns] = lbx;
-            S->off[ns] = n;
-            S->len[ns] = m;
-            S->leaf[ns] = lf;
-          }
-          n += mp;
-          ++ns;
-        }
-      }
-    }
-    if (ns > 0) commit(ns);
-    __syncwarp();
-    if (lane == 0) {
-      S->nseg = -1;
-      mbar_arrive(&W.full[itn % kRS]);
-    }
-    return;
-  }
-
-  // ================= consumers =================
-  u64(*q)[32] = W.q[cw];
-  unsigned long long nev = 0;
-  // pre-pass: this warp's own leaves (the leaves holding its 32 queries), staged privately
-  int xa = 0x7fffffff, xb = -1;
-  if (wact) {
-    const int qb = q0 + cw * 32, qend = min(qb + 32, qhi);
-    for (int l0 = LJa; l0 < LJb; l0 += 32) {
-      const int l = l0 + lane;
-      const bool ov = l < LJb && a.leaf_beg[l] < qend && a.leaf_beg[l + 1] > qb;
-      const unsigned b = __ballot_sync(0xffffffffu, ov);
-      if (b) {
-        xa = min(xa, l0 + __ffs(b) - 1);
-        xb = max(xb, l0 + 32 - __clz(b));
-      }
-    }
-    Slot &O = W.own[cw];
-    int n = 0, ns = 0;
-    for (int lf = xa; lf < xb; ++lf) {
-      const int lp = a.leaf_beg[lf], m = a.leaf_beg[lf + 1] - lp, mp = (m + 3) & ~3;
-      if (n + mp > kSCap || ns == kSSeg) {
-        __syncwarp();
-        wslot<K, PER>(a, D, O, ns, -1, -1, wbox, qx, qy, qz, act, q, L, nev);
-        __syncwarp();
-        n = ns = 0;
-      }
-      for (int t = lane; t < mp; t += 32) {
-        float4 p = make_float4(__int_as_float(0x7fc00000), __int_as_float(0x7fc00000), __int_as_float(0x7fc00000), 0.f);
-        if (t < m) p = a.pts[lp + t];
-        O.x[n + t] = p.x;
-        O.y[n + t] = p.y;
-        O.z[n + t] = p.z;
-        O.g[n + t] = __float_as_int(p.w);
-      }
-      if (lane == 0) {
-        O.box[ns] = a.leaf_box[lf];
-        O.off[ns] = n;
-        O.len[ns] = m;
-        O.leaf[ns] = lf;
-      }
-      n += mp;
-      ++ns;
-    }
-    __syncwarp();
-    if (ns) wslot<K, PER>(a, D, O, ns, -1, -1, wbox, qx, qy, qz, act, q, L, nev);
-    const float wmk = warp_max_kth(L.kth);
-    if (lane == 0) W.wmax[cw] = wmk;
-  }
-  for (int itn = 0;; ++itn) {
-    const int sl = itn % kRS;
-    mbar_wait(&W.full[sl], (itn / kRS) & 1);
-    const Slot &S = W.ring[sl];
-    const int ns = S.nseg;
-    if (ns < 0) break;
-    if (wact) {
-      wslot<K, PER>(a, D, S, ns, xa, xb, wbox, qx, qy, qz, act, q, L, nev);
-      const float wmk = warp_max_kth(L.kth);  // all lanes (warp reduction)
-      if (lane == 0) W.wmax[cw] = wmk;
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&W.empty[sl]);
-  }
-  if (a.stats) {
-    unsigned long long tot = nev, ins = L.ins;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      tot += __shfl_xor_sync(0xffffffffu, tot, o);
-      ins += __shfl_xor_sync(0xffffffffu, ins, o);
-    }
-    if (lane == 0) {
-      atomicAdd(&a.stats[0], tot);
-      atomicAdd(&a.stats[1], ins);
-    }
-  }
-  if (act) {
-    const int64_t row = a.order == JZ_ORDER_INPUT ? (int64_t)inpos : (a.zrow ? (int64_t)a.zrow[qi] : (int64_t)qi);
-    int32_t *oi = a.out_idx + row * a.k;
-    float *od = a.out_d2 + row * a.k;
+    int32_t *oi = a.out_idx + row * a.ldo + a.col0;
+    float *od = a.out_d2 + row * a.ldo + a.col0;
 #pragma unroll
     for (int j = 0; j < K; ++j) {
       if (j >= K - a.k) {
@@ -864,21 +444,14 @@ __global__ void k_item_fill(const int32_t *__restrict__ par_leaf, const int32_t 
 }
 
 template <int K>
-static void launch_ws(const LeafPK &la, const ItemWS &iw, const Dom &D, cudaStream_t st) {
-  const size_t smem = sizeof(WSShared);
-  if (D.periodic) {
-    JZ_CUDA(cudaFuncSetAttribute(k_leafws<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_leafws<K, true><<<(unsigned)iw.nitems, kWThreads, smem, st>>>(la, iw, D);
-  } else {
-    JZ_CUDA(cudaFuncSetAttribute(k_leafws<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_leafws<K, false><<<(unsigned)iw.nitems, kWThreads, smem, st>>>(la, iw, D);
-  }
-}
-
-template <int K>
 static void launch_l(const LeafPK &la, const Dom &D, unsigned blocks, cudaStream_t st) {
-  if (D.periodic) k_leaf<K, true><<<blocks, kLThreads, 0, st>>>(la, D);
-  else k_leaf<K, false><<<blocks, kLThreads, 0, st>>>(la, D);
+  if (la.col0 > 0) {  // later pass of a k > k_max query
+    if (D.periodic) k_leaf<K, true, true><<<blocks, kLThreads, 0, st>>>(la, D);
+    else k_leaf<K, true, false><<<blocks, kLThreads, 0, st>>>(la, D);
+  } else {
+    if (D.periodic) k_leaf<K, false, true><<<blocks, kLThreads, 0, st>>>(la, D);
+    else k_leaf<K, false, false><<<blocks, kLThreads, 0, st>>>(la, D);
+  }
 }
 
 void leaf_to_leaf(const LeafArgs &a, const Dom &D, cudaStream_t st) {
@@ -887,21 +460,23 @@ void leaf_to_leaf(const LeafArgs &a, const Dom &D, cudaStream_t st) {
   int64_t *off = nullptr;
   JZ_CUDA(cudaMallocAsync(&cnt, a.npar * sizeof(int32_t), st));
   JZ_CUDA(cudaMallocAsync(&off, (a.npar + 1) * sizeof(int64_t), st));
-  const bool ws = (a.flags & JZ_FLAG_WS_LEAF) != 0;  // experimental warp-specialised variant
-  const int chunk = ws ? kWC * 32 : 32;
-  k_item_count<<<grid_for(a.npar, 256), 256, 0, st>>>(a.par_leaf, a.leaf_beg, a.npar, chunk, cnt);
+  const int chunk = 32;
+  k_item_count<<<grid_for(a.npar, 256), 256, 0, st>>>(a.par_leaf, a.qbeg, a.npar, chunk, cnt);
   JZ_LAUNCH_CHECK();
   exclusive_scan_i32_to_i64(cnt, off, a.npar, st);
   const int64_t nitems = read_i64(off + a.npar, st);
   int32_t *item_par = nullptr, *item_q0 = nullptr;
   JZ_CUDA(cudaMallocAsync(&item_par, (nitems + 1) * sizeof(int32_t), st));
   JZ_CUDA(cudaMallocAsync(&item_q0, (nitems + 1) * sizeof(int32_t), st));
-  k_item_fill<<<grid_for(a.npar, 256), 256, 0, st>>>(a.par_leaf, a.leaf_beg, a.npar, chunk, off, item_par, item_q0);
+  k_item_fill<<<grid_for(a.npar, 256), 256, 0, st>>>(a.par_leaf, a.qbeg, a.npar, chunk, off, item_par, item_q0);
   JZ_LAUNCH_CHECK();
 
   LeafPK la;
-  la.pts = a.pts;
-  la.leaf_beg = a.leaf_beg;
+  la.spts = a.spts;
+  la.sbeg = a.sbeg;
+  la.qpts = a.qpts;
+  la.qbeg = a.qbeg;
+  la.qin = a.qin;
   la.leaf_box = a.leaf_box;
   la.par_leaf = a.par_leaf;
   la.par_box = a.par_box;
@@ -912,10 +487,7 @@ void leaf_to_leaf(const LeafArgs &a, const Dom &D, cudaStream_t st) {
   la.item_par = item_par;
   la.item_q0 = item_q0;
   la.nitems = nitems;
-  la.perm = a.perm;
-  la.zrow = a.zrow;
-  la.n_query = a.n_query;
-  la.k = a.k;
+  la.ldo = a.k;
   la.order = a.order;
   la.early = !(a.flags & JZ_FLAG_NO_EARLY_EXIT);
   la.sorted = !(a.flags & (JZ_FLAG_NO_SEGSORT | JZ_FLAG_NO_EARLY_EXIT));
@@ -923,20 +495,18 @@ void leaf_to_leaf(const LeafArgs &a, const Dom &D, cudaStream_t st) {
   la.out_d2 = a.out_d2;
   la.out_row_gidx = a.out_row_gidx;
   la.stats = a.evals;
-  la.seed_d2 = nullptr;
   if (nitems > 0) {
-    if (ws) {
-      ItemWS iw{item_par, item_q0, nitems};
-      if (a.k <= 8) launch_ws<8>(la, iw, D, st);
-      else if (a.k <= 16) launch_ws<16>(la, iw, D, st);
-      else launch_ws<32>(la, iw, D, st);
-    } else {
-      const unsigned blocks = (unsigned)ceil_div(nitems, kLWarps);
-      if (a.k <= 8) launch_l<8>(la, D, blocks, st);
-      else if (a.k <= 16) launch_l<16>(la, D, blocks, st);
+    const unsigned blocks = (unsigned)ceil_div(nitems, kLWarps);
+    // k > k_max: ceil(k / k_max) passes over the same interaction list (built for R_max(k));
+    // pass c keeps only keys after the last (d2, index) of pass c-1.
+    for (int c0 = 0; c0 < a.k; c0 += kMaxK) {
+      la.col0 = c0;
+      la.k = a.k - c0 < kMaxK ? a.k - c0 : kMaxK;
+      if (la.k <= 8) launch_l<8>(la, D, blocks, st);
+      else if (la.k <= 16) launch_l<16>(la, D, blocks, st);
       else launch_l<32>(la, D, blocks, st);
+      JZ_LAUNCH_CHECK();
     }
-    JZ_LAUNCH_CHECK();
   }
   JZ_CUDA(cudaFreeAsync(cnt, st));
   JZ_CUDA(cudaFreeAsync(off, st));

@@ -12,7 +12,8 @@ from synth import clustered_points, uniform_points  # noqa: E402
 
 
 @pytest.mark.parametrize("R", [1, 2, 4, 8])
-@pytest.mark.parametrize("kind,box,k", [("clustered", 1.0, 16), ("uniform", None, 8), ("clustered", None, 32)])
+@pytest.mark.parametrize("kind,box,k", [("clustered", 1.0, 16), ("uniform", None, 8), ("clustered", None, 32),
+                                        ("clustered", 1.0, 48)])
 def test_simulated_ranks_equal_oracle(R, kind, box, k):
     from paper_2604_05885_b200.dist import run_ranks_simulated
 

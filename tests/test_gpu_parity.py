@@ -22,10 +22,11 @@ def _jz():
     return jz
 
 
-def _gpu_knn(pos, k, box, order="input", params=None):
+def _gpu_knn(pos, k, box, order="input", params=None, queries=None):
     jz = _jz()
     t = torch.from_numpy(np.ascontiguousarray(pos, dtype=np.float32)).cuda()
-    ix = jz.KnnIndex(t, box=box, params=params)
+    q = None if queries is None else torch.from_numpy(np.ascontiguousarray(queries, dtype=np.float32)).cuda()
+    ix = jz.KnnIndex(t, box=box, params=params, queries=q)
     out = ix.query(k, order=order)
     res = tuple(o.cpu().numpy() for o in out)
     ix.free()
@@ -120,17 +121,6 @@ def test_pruning_safety():
         assert np.array_equal(ref[0], got[0]) and np.array_equal(ref[1].view(np.int32), got[1].view(np.int32))
 
 
-@pytest.mark.parametrize("box,k", [(1.0, 16), (None, 8), (1.0, 32)])
-def test_parity_warp_specialised_variant(box, k):
-    """The experimental warp-specialised LeafToLeaf (producer warp + mbarrier ring) gives the
-    same bits as the default kernel and the oracle."""
-    jz = _jz()
-    pos = clustered_points(60000, 31, 1.0)
-    ig, dg = _gpu_knn(pos, k, box, params=dict(flags=jz.JZ_FLAG_WS_LEAF))
-    io, do = knn_grid(pos, k, box)
-    _assert_same(ig, dg, io, do)
-
-
 def test_z_order_rows():
     pos = uniform_points(20000, 9, 1.0)
     ii, di = _gpu_knn(pos, 8, 1.0)
@@ -167,7 +157,7 @@ def test_errors():
     jz = _jz()
     good = torch.from_numpy(uniform_points(100, 12, 1.0)).cuda()
     with pytest.raises(jz.JzError) as e:
-        jz.knn(good, 33, box=1.0)
+        jz.knn(good, 101, box=1.0)
     assert e.value.code == 2
     with pytest.raises(jz.JzError) as e:
         jz.knn(good[:5], 6, box=1.0)
@@ -291,3 +281,120 @@ def test_c4_full_size_sampled():
     tie = d2[:, 1:] == d2[:, :-1]
     assert bool((idx[:, 1:][tie] > idx[:, :-1][tie]).all())
     assert bool((d2[:, 0] == 0).all())
+
+
+# ----------------------------------------------------------------------------------- F1
+# separate query points (joint tree over both types)
+# and k > k_max = 32 (ceil(k/32) LeafToLeaf passes with the (d2, index) lower bound, L386).
+
+
+def _q_sets():
+    yield "uniform", uniform_points(6000, 201, 1.0), uniform_points(4000, 202, 1.0), 1.0
+    yield "clustered-src-uniform-q", clustered_points(20000, 203, 1.0), uniform_points(9000, 204, 1.0), 1.0
+    yield "uniform-src-clustered-q", uniform_points(5000, 205, 1.0), clustered_points(30000, 206, 1.0), 1.0
+    yield "open-q-outside-hull", clustered_points(12000, 207, 1.0), uniform_points(5000, 208, 1.0) * 3 - 1, None
+    yield "few-q", clustered_points(40000, 209, 1.0), uniform_points(7, 210, 1.0), None
+    yield "few-src", uniform_points(40, 211, 1.0), clustered_points(20000, 212, 1.0), 1.0
+    yield "lattice-ties", lattice_points(16, 1.0 / 16), lattice_points(8, 1.0 / 8) + np.float32(1.0 / 32), 1.0
+    yield "anisotropic", (uniform_points(8000, 213, 1.0) * np.array([2.0, 1.0, 0.5], np.float32)), \
+        (uniform_points(3000, 214, 1.0) * np.array([2.0, 1.0, 0.5], np.float32)), (2.0, 1.0, 0.5)
+
+
+@pytest.mark.parametrize("name,src,qry,box", list(_q_sets()), ids=[s[0] for s in _q_sets()])
+@pytest.mark.parametrize("k", [1, 8, 16, 32])
+def test_separate_queries_parity(name, src, qry, box, k):
+    if k > len(src):
+        pytest.skip("k > n_src")
+    ig, dg = _gpu_knn(src, k, box, queries=qry)
+    io, do = knn_grid(src, k, box, queries=qry)
+    _assert_same(ig, dg, io, do)
+
+
+def test_separate_queries_small_brute():
+    """Sizes spanning the ragged cases: one query, one source, queries == k sources."""
+    for ns, nq, k in [(1, 1, 1), (1, 5, 1), (5, 1, 5), (33, 100, 33), (3073, 129, 16), (100, 3073, 100)]:
+        for box in (1.0, None):
+            src = uniform_points(ns, 300 + ns, 1.0)
+            qry = uniform_points(nq, 400 + nq, 1.0)
+            ig, dg = _gpu_knn(src, k, box, queries=qry)
+            io, do = knn_brute(src, k, box, queries=qry)
+            _assert_same(ig, dg, io, do)
+
+
+def test_separate_queries_z_order_and_empty():
+    jz = _jz()
+    src = clustered_points(20000, 215, 1.0)
+    qry = uniform_points(7000, 216, 1.0)
+    ii, di = _gpu_knn(src, 8, 1.0, queries=qry)
+    iz, dz, gz = _gpu_knn(src, 8, 1.0, order="z", queries=qry)
+    assert sorted(gz.tolist()) == list(range(7000))  # z rows name the query row
+    assert np.array_equal(iz, ii[gz]) and np.array_equal(dz, di[gz])
+    t = torch.from_numpy(src).cuda()
+    ix = jz.KnnIndex(t, box=1.0, queries=torch.empty((0, 3), device="cuda"))
+    idx, d2 = ix.query(8)
+    assert idx.shape == (0, 8)
+    with pytest.raises(jz.JzError) as e:  # k > number of sources
+        jz.knn(t[:10], 11, box=1.0, queries=torch.from_numpy(qry).cuda())
+    assert e.value.code == 2
+
+
+def test_xyzg_point_types():
+    """jz_knn_build_xyzg type rule: query iff input position < n_query, source iff gidx >= 0
+    (a query-only point has gidx < 0; ghosts are source-only points after n_query)."""
+    jz = _jz()
+    pos = clustered_points(30000, 217, 1.0)
+    nq = 18000
+    r = np.random.default_rng(5)
+    is_src = np.ones(len(pos), bool)
+    is_src[:nq] = r.random(nq) < 0.5  # half of the queries are also sources
+    gidx = np.full(len(pos), -1, np.int64)
+    gidx[is_src] = np.arange(is_src.sum()) * 3 + 7  # monotone in source order: same tie order
+    pts4 = np.concatenate([pos, gidx.astype(np.int32).view(np.float32)[:, None]], axis=1)
+    ix = jz.KnnIndex(torch.from_numpy(np.ascontiguousarray(pts4)).cuda(), box=1.0, n_query=nq)
+    idx, d2 = ix.query(16)
+    _, _, rg = ix.query(16, order="z")
+    io, do = knn_grid(pos[is_src], 16, 1.0, queries=pos[:nq])
+    _assert_same(idx.cpu().numpy(), d2.cpu().numpy(), gidx[is_src][io].astype(np.int32), do)
+    # z rows name the query: its gidx when it is also a source, else its input row
+    exp = np.where(is_src[:nq], gidx[:nq], np.arange(nq))
+    assert np.array_equal(np.sort(rg.cpu().numpy()), np.sort(exp.astype(np.int32)))
+
+
+@pytest.mark.parametrize("k", [33, 48, 64, 100, 257])
+@pytest.mark.parametrize("box", [1.0, None])
+def test_large_k_parity(k, box):
+    pos = clustered_points(20000, 218, 1.0)
+    ig, dg = _gpu_knn(pos, k, box)
+    io, do = knn_grid(pos, k, box)
+    _assert_same(ig, dg, io, do)
+
+
+@pytest.mark.parametrize("k", [40, 96])
+def test_large_k_ties_and_separate_queries(k):
+    """k > 32 on a lattice (many equal distances: the index offset of the pass boundary
+    decides) and with separate queries."""
+    pos = lattice_points(16, 1.0 / 16)
+    ig, dg = _gpu_knn(pos, k, 1.0)
+    io, do = knn_brute(pos, k, 1.0)
+    _assert_same(ig, dg, io, do)
+    src, qry = clustered_points(30000, 219, 1.0), uniform_points(5000, 220, 1.0)
+    ig, dg = _gpu_knn(src, k, 1.0, queries=qry)
+    io, do = knn_grid(src, k, 1.0, queries=qry)
+    _assert_same(ig, dg, io, do)
+
+
+def test_separate_queries_full_size_sampled():
+    """10^7 clustered sources + 10^7 uniform queries (periodic, k = 16): 20000 sampled rows
+    vs the grid oracle, invariants on every row."""
+    jz = _jz()
+    src, box, k = make_config("C3")
+    src = src[:10**7]
+    qry = uniform_points(10**7, 221, 1.0)
+    ix = jz.KnnIndex(torch.from_numpy(src).cuda(), box=box, queries=torch.from_numpy(qry).cuda())
+    idx, d2 = ix.query(16)
+    rows = np.random.default_rng(9).choice(10**7, 20000, replace=False)
+    io, do = knn_grid(src, 16, box, rows=rows, queries=qry)
+    _assert_same(idx[rows].cpu().numpy(), d2[rows].cpu().numpy(), io, do)
+    d = d2.double()
+    assert bool((d[:, 1:] >= d[:, :-1]).all()) and bool(torch.isfinite(d).all())
+    assert int(idx.min()) >= 0 and int(idx.max()) < 10**7
