@@ -340,6 +340,7 @@ int jz_knn_query(jz_knn_index *ix, int k, int order, int32_t *out_idx, float *ou
   la.qbeg = ix->qbeg;
   la.qin = ix->qin;
   la.leaf_box = ix->planes[0].box;
+  la.nleaf = ix->planes[0].nnodes;
   la.par_leaf = one_plane ? superbeg : ix->planes[1].beg;
   la.par_box = one_plane ? nullptr : ix->planes[1].box;
   la.npar = il.nrecv;

@@ -64,6 +64,7 @@ struct LeafArgs {
   const int32_t *qbeg;      // [nleaf+1] first query of each leaf
   const int32_t *qin;       // [nq] input row of each query
   const NodeBox *leaf_box;  // [nleaf]
+  int64_t nleaf;
   const int32_t *par_leaf;  // [npar+1] first leaf of each receiving parent
   const NodeBox *par_box;   // [npar] or nullptr
   int64_t npar;

@@ -6,8 +6,11 @@
 //    The item walks J's plane-1 interaction list (sorted by r_low): the leaf-level
 //    NodeToNode pass is not materialised. Leaf pairs are pruned on the fly: the bounding box
 //    of the warp's queries is tested against each source node S and then, one lane per child
-//    leaf, against S's child leaves (a ballot gives the survivors), with the exact monotone
-//    d_low^2 bound against the warp's current max k-th distance (the early exit of P:L398).
+//    leaf, against S's child leaves (a ballot gives the survivors), and every lane tests its
+//    own query against each survivor (the early exit of P:L398, per lane).
+//  * Pruning bounds use centre / half-extent boxes whose extents carry an absolute rounding
+//    margin, and the bound is scaled by (1 - 2^-19): branch-free, and never above the
+//    canonical d2 of any pair in the boxes (R8b).
 //  * Surviving leaves are staged by the warp into its own shared-memory slot as separate
 //    x / y / z / gidx arrays (coalesced 16-byte loads, leaf starts aligned to 4, tails padded
 //    with NaN coordinates so their d2 is NaN and never passes a comparison).
@@ -15,10 +18,13 @@
 //    operand: FADD2 x3, FMUL2, FFMA2 x2 per source pair = the canonical scalar formula with
 //    per-element round-to-nearest (bit-identical). Periodic leaf pairs whose pairs all wrap
 //    the same way get one extra exact FADD2 per axis; straddling pairs use the per-pair select.
-//  * Filtering: per group of 4 sources the lane compares min(d2) with its k-th distance; the
-//    insertion slow path runs only when some lane passes. Top-k: sorted register list of
-//    64-bit keys (d2_bits << 32 | gidx + 1): unsigned order == (d2, index) order (R2),
-//    initialised with sentinels at R_max^2 of J (bounds every contained query's k-th distance).
+//  * Top-k: each lane keeps the K smallest d2 VALUES in a sorted register
+//    list updated by a min/max bubble (2 FMNMX per slot, no predicates) and appends every
+//    candidate with d2 <= its current k-th value to a lane-private log in shared memory
+//    (key = d2_bits << 32 | gidx + 1, so unsigned order == (d2, index) order, R2).
+//    The log is compacted to the entries <= the current k-th value when it fills; at the end
+//    the k smallest keys of the log are the row (bitonic sort in registers). The list starts
+//    full of R_max^2(J), which bounds every contained query's k-th distance.
 //  * Rows are written straight to their final place (input or z order): no reorder pass.
 #include "jz_common.cuh"
 #include "jz_internal.h"
@@ -28,7 +34,11 @@ namespace jz {
 constexpr int kLWarps = 2;
 constexpr int kLThreads = kLWarps * 32;
 constexpr int kLCap = 256;  // staged source points per warp (4 KB SoA)
-constexpr int kQCap = 16;   // per-lane candidate queue (4 KB per warp)
+
+template <int K>
+struct LogCap {
+  static constexpr int C = K + 16;  // log entries per lane
+};
 
 typedef unsigned long long u64;
 
@@ -61,136 +71,185 @@ __device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c) {
   return d;
 }
 
-// Sorted insert of `key` (known to be < a[K-1]) into a[0..K). The list is cut into quarters;
-// a quarter is touched only if key < its last element, so the common late insertion near the
-// tail costs one quarter of the compare/select network.
-template <int K>
-__device__ __forceinline__ void topk_insert(u64 (&a)[K], u64 key) {
-  constexpr int Q = K / 4;
-#pragma unroll
-  for (int q = 3; q >= 0; --q) {
-    if (key < a[q * Q + Q - 1]) {
-#pragma unroll
-      for (int j = q * Q + Q - 1; j >= q * Q; --j) {
-        const bool mv = j > 0 && key < a[j > 0 ? j - 1 : 0];
-        a[j] = mv ? a[j > 0 ? j - 1 : 0] : (key < a[j] ? key : a[j]);
-      }
-    }
-  }
-}
-
-struct LeafPK {
-  const float4 *spts;        // source points, z order (type-separated, P:L279)
-  const int32_t *sbeg;       // [nleaf+1] first source of each leaf
-  const float4 *qpts;        // query points, z order
-  const int32_t *qbeg;       // [nleaf+1] first query of each leaf
-  const int32_t *qin;        // [nq] input row of each query
-  const NodeBox *leaf_box;   // [nleaf]
-  const int32_t *par_leaf;   // [npar+1] first leaf of each receiving parent
-  const NodeBox *par_box;    // [npar] or nullptr
-  const int64_t *ispl;       // parent-level interaction list
-  const int32_t *isrc;
-  const float *rlow;
-  const float *rmax2;        // [npar] or nullptr (= +inf)
-  const int32_t *item_par;   // [nitems] receiving parent of each 32-query work item
-  const int32_t *item_q0;    // [nitems] first query (sorted position) of the item
-  int64_t nitems;
-  int k;      // neighbours found by this pass (<= K)
-  int col0;   // first output column of this pass (k > k_max chunking)
-  int ldo;    // output row stride (total k)
-  int order;
-  int early;
-  int sorted;
-  int32_t *out_idx;
-  float *out_d2;
-  int32_t *out_row_gidx;
-  unsigned long long *stats;  // [0] distance evaluations, [1] top-k insertions (or nullptr)
+// ---------------------------------------------------------------- pruning bounds
+// Box as centre c and half extent e, e including an absolute margin m >= 2^-18 * (largest
+// coordinate magnitude of the box, or L when periodic). For any q in box A and s in box B the
+// canonical per-axis difference t = wrap(RN(q - s)) satisfies |t| >= gap = max(0, |c_A - c_B|
+// (minimal image) - e_A - e_B): the margin absorbs the rounding of c, e, RN(q - s) and of the
+// gap itself. The sum of squares is then scaled by (1 - 2^-19) to absorb the relative error
+// of the rounded squares, so dlow2 <= canonical d2(q, s) for every pair (R8b).
+struct CE {
+  float4 c;  // centre (w unused)
+  float4 e;  // half extent + margin (w unused)
 };
 
-// per-axis shift class of a (query box, source box) pair: 0 = no wrap for any pair,
-// 1 = every pair wraps by -L, 2 = every pair wraps by +L (shift returned in sh),
-// 3 = straddles (per-pair select)
-__device__ __forceinline__ int shift_class(float qlo, float qhi, float slo, float shi, float L, float h, float &sh) {
-  const float tmin = __fsub_rn(qlo, shi), tmax = __fsub_rn(qhi, slo);
-  sh = 0.f;
-  if (tmin >= h) {
-    sh = -L;
-    return 1;
-  }
-  if (tmax < -h) {
-    sh = L;
-    return 2;
-  }
-  if (tmin >= -h && tmax < h) return 0;
+constexpr float kLowScale = 1.0f - 1.0f / 524288.0f;  // 1 - 2^-19
+
+template <bool PER>
+__device__ __forceinline__ float gap1(float dc, float E, float L) {
+  float a = fabsf(dc);
+  if (PER) a = fminf(a, __fsub_rn(L, a));
+  return fmaxf(__fsub_rn(a, E), 0.f);
+}
+
+template <bool PER>
+__device__ __forceinline__ float dlow2_ce(float dcx, float dcy, float dcz, float Ex, float Ey, float Ez, const Dom &D) {
+  const float gx = gap1<PER>(dcx, Ex, D.L[0]);
+  const float gy = gap1<PER>(dcy, Ey, D.L[1]);
+  const float gz = gap1<PER>(dcz, Ez, D.L[2]);
+  return __fmul_rn(__fmaf_rn(gz, gz, __fmaf_rn(gy, gy, __fmul_rn(gx, gx))), kLowScale);
+}
+
+// per-axis periodic shift class of a box pair from the signed centre difference dc and the
+// summed extents E (margins included): every pair's RN(q - s) lies in [dc - E, dc + E].
+// 0 = no pair wraps, 1 = every pair wraps by -L, 2 = every pair wraps by +L, 3 = straddles.
+__device__ __forceinline__ int ce_class(float dc, float E, float h) {
+  const float tlo = __fsub_rn(dc, E), thi = __fadd_rn(dc, E);
+  if (tlo >= h) return 1;
+  if (thi < -h) return 2;
+  if (tlo >= -h && thi < h) return 0;
   return 3;
 }
 
 __device__ __forceinline__ bool any_straddle(int c) {
   return ((c & 3) == 3) || (((c >> 2) & 3) == 3) || (((c >> 4) & 3) == 3);
 }
+__device__ __forceinline__ float class_shift(int c, float L) { return c == 1 ? -L : (c == 2 ? L : 0.f); }
 
+__device__ __forceinline__ float ce_margin(float lx, float ly, float lz, float hx, float hy, float hz, float Lmax) {
+  float m = fmaxf(fmaxf(fmaxf(fabsf(lx), fabsf(hx)), fmaxf(fabsf(ly), fabsf(hy))), fmaxf(fabsf(lz), fabsf(hz)));
+  return __fmul_ru(fmaxf(m, Lmax), 1.0f / 262144.0f);  // 2^-18
+}
+
+__device__ __forceinline__ CE make_ce(float lx, float ly, float lz, float hx, float hy, float hz, float Lmax) {
+  const float m = ce_margin(lx, ly, lz, hx, hy, hz, Lmax);
+  CE r;
+  r.c = make_float4(__fmul_rn(__fadd_rn(lx, hx), 0.5f), __fmul_rn(__fadd_rn(ly, hy), 0.5f),
+                    __fmul_rn(__fadd_rn(lz, hz), 0.5f), 0.f);
+  r.e = make_float4(__fadd_ru(__fmul_ru(__fsub_ru(hx, lx), 0.5f), m), __fadd_ru(__fmul_ru(__fsub_ru(hy, ly), 0.5f), m),
+                    __fadd_ru(__fmul_ru(__fsub_ru(hz, lz), 0.5f), m), 0.f);
+  return r;
+}
+
+__global__ void k_box_ce(const NodeBox *__restrict__ box, int64_t n, float Lmax, CE *__restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const NodeBox b = box[i];
+    out[i] = make_ce(b.lo.x, b.lo.y, b.lo.z, b.hi.x, b.hi.y, b.hi.z, Lmax);
+  }
+}
+
+// ---------------------------------------------------------------- top-k state
+template <int K>
+__device__ __forceinline__ void bubble(float (&F)[K], float d) {
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    const float lo = fminf(F[j], d);
+    d = fmaxf(F[j], d);
+    F[j] = lo;
+  }
+}
+
+template <int K>
 struct WarpBuf {
   float x[kLCap], y[kLCap], z[kLCap];
   int g[kLCap];
-  u64 q[kQCap][32];  // candidate queue, lane-minor
+  u64 log[LogCap<K>::C][32];  // lane-minor: conflict-free
 };
 
 template <int K, bool LB>
 struct Lane {
-  u64 tk[K];
-  u64 lb;    // keys <= lb were found by earlier passes (0 on the first pass)
-  float kth;
+  float F[K];  // K smallest d2 values seen (ascending); F[K-1] = current k-th value
+  u64 lb;      // keys <= lb were found by earlier passes (0 on the first pass)
+  float kth;   // F[K-1] (inactive lanes: -1, never passes a comparison)
+  int nl;      // log entries
+  int nf;      // log entries already merged into F
   unsigned ins;
-  int qn;    // queued candidates
-  bool act;  // lane holds a query (inactive lanes keep kth = -1)
+  bool act;
 };
 
-// Insert the lane's queued candidates: all lanes drain their queues in parallel, so the
-// warp runs max(queue length) insertion rounds instead of one per candidate group.
+// merge the lane's new log entries into F (all lanes in lockstep: max(new) rounds)
 template <int K, bool LB>
-__device__ __forceinline__ void flush(WarpBuf &B, Lane<K, LB> &L) {
+__device__ __forceinline__ void merge(WarpBuf<K> &B, Lane<K, LB> &L) {
   const int lane = threadIdx.x & 31;
-  const int mx = __reduce_max_sync(0xffffffffu, (unsigned)L.qn);
-  for (int i = 0; i < mx; ++i) {
-    if (i < L.qn) {
-      const u64 key = B.q[i][lane];
-      if (key < L.tk[K - 1]) {
-        topk_insert<K>(L.tk, key);
-        ++L.ins;
-      }
-    }
-  }
-  L.kth = L.act ? __uint_as_float((unsigned)(L.tk[K - 1] >> 32)) : -1.f;
-  L.qn = 0;
-}
-
-template <int K, bool LB>
-__device__ __forceinline__ void cand(Lane<K, LB> &L, float d2, int g) {
-  if (d2 <= L.kth) {
-    const u64 key = ((u64)__float_as_uint(d2) << 32) | (unsigned)(g + 1);
-    if (key < L.tk[K - 1] && (!LB || key > L.lb)) {
-      topk_insert<K>(L.tk, key);
-      L.kth = __uint_as_float((unsigned)(L.tk[K - 1] >> 32));
+  const int r0 = (int)__reduce_min_sync(0xffffffffu, (unsigned)L.nf);
+  const int r1 = (int)__reduce_max_sync(0xffffffffu, (unsigned)L.nl);
+  for (int r = r0; r < r1; ++r) {
+    float d = INFINITY;
+    if (r >= L.nf && r < L.nl) d = __uint_as_float((unsigned)(B.log[r][lane] >> 32));
+    if (d < L.F[K - 1]) {
+      bubble<K>(L.F, d);
       ++L.ins;
     }
   }
+  L.nf = L.nl;
+  L.kth = L.act ? L.F[K - 1] : -1.f;
+}
+
+// keep only the log entries with d2 <= k-th value; with massive exact ties at the k-th value
+// drop the largest keys until K remain (they cannot be among the K smallest keys)
+template <int K>
+__device__ __noinline__ int drop_largest(WarpBuf<K> &B, int nl, int keep) {
+  const int lane = threadIdx.x & 31;
+  while (nl > keep) {
+    int im = 0;
+    u64 mk = 0;
+    for (int r = 0; r < nl; ++r) {
+      const u64 e = B.log[r][lane];
+      if (e > mk) {
+        mk = e;
+        im = r;
+      }
+    }
+    B.log[im][lane] = B.log[nl - 1][lane];
+    --nl;
+  }
+  return nl;
 }
 
 template <int K, bool LB>
-__device__ __forceinline__ void enqueue(WarpBuf &B, Lane<K, LB> &L, float d2, int g) {
+__device__ __forceinline__ void compact(WarpBuf<K> &B, Lane<K, LB> &L) {
+  constexpr int C = LogCap<K>::C;
+  const int lane = threadIdx.x & 31;
+  merge<K, LB>(B, L);
+  const unsigned kb = __float_as_uint(L.kth);
+  const int r1 = (int)__reduce_max_sync(0xffffffffu, (unsigned)L.nl);
+  int j = 0;
+  for (int r = 0; r < r1; ++r) {
+    if (r < L.nl) {
+      const u64 e = B.log[r][lane];
+      if ((unsigned)(e >> 32) <= kb) {
+        B.log[j][lane] = e;
+        ++j;
+      }
+    }
+  }
+  L.nl = L.nf = j;
+  if (__any_sync(0xffffffffu, j > C - 8)) L.nl = L.nf = drop_largest<K>(B, L.nl, K);
+}
+
+template <int K, bool LB>
+__device__ __forceinline__ void append(WarpBuf<K> &B, Lane<K, LB> &L, float d2, int g) {
   if (d2 <= L.kth) {
     const u64 key = ((u64)__float_as_uint(d2) << 32) | (unsigned)(g + 1);
     if (!LB || key > L.lb) {
-      B.q[L.qn][threadIdx.x & 31] = key;
-      ++L.qn;
+      B.log[L.nl][threadIdx.x & 31] = key;
+      ++L.nl;
     }
   }
 }
 
-// evaluate staged sources [0, n) (n multiple of 4, NaN padded) against the lane's query
+template <int K, bool LB>
+__device__ __forceinline__ void append_chk(WarpBuf<K> &B, Lane<K, LB> &L, float d2, int g) {
+  append<K, LB>(B, L, d2, g);
+  if (__any_sync(0xffffffffu, L.nl > LogCap<K>::C - 4)) compact<K, LB>(B, L);  // keep nl <= C - 4 between groups
+}
+
+// ---------------------------------------------------------------- distance evaluation
+// staged sources [0, n) (n multiple of 4, NaN padded) against the lane's query
 template <int K, bool LB, bool SHIFT>
-__device__ __forceinline__ void eval_block(WarpBuf &B, int n, float qx, float qy, float qz, float shx, float shy,
+__device__ __forceinline__ void eval_block(WarpBuf<K> &B, int n, float qx, float qy, float qz, float shx, float shy,
                                            float shz, Lane<K, LB> &L) {
+  constexpr int C = LogCap<K>::C;
   const u64 QX = pk(qx, qx), QY = pk(qy, qy), QZ = pk(qz, qz);
   const u64 SX = pk(shx, shx), SY = pk(shy, shy), SZ = pk(shz, shz);
   for (int j = 0; j < n; j += 4) {
@@ -216,67 +275,108 @@ __device__ __forceinline__ void eval_block(WarpBuf &B, int n, float qx, float qy
     const float m = fminf(fminf(a0, a1), fminf(a2, a3));  // NaN padding is ignored by min
     if (__any_sync(0xffffffffu, m <= L.kth)) {
       const int4 G = *reinterpret_cast<const int4 *>(&B.g[j]);
-      enqueue<K, LB>(B, L, a0, G.x);
-      enqueue<K, LB>(B, L, a1, G.y);
-      enqueue<K, LB>(B, L, a2, G.z);
-      enqueue<K, LB>(B, L, a3, G.w);
-      if (__any_sync(0xffffffffu, L.qn > kQCap - 4)) flush<K, LB>(B, L);
+      append<K, LB>(B, L, a0, G.x);
+      append<K, LB>(B, L, a1, G.y);
+      append<K, LB>(B, L, a2, G.z);
+      append<K, LB>(B, L, a3, G.w);
+      if (__any_sync(0xffffffffu, L.nl > C - 4)) compact<K, LB>(B, L);
     }
   }
-  if (__any_sync(0xffffffffu, L.qn > 0)) flush<K, LB>(B, L);
+  merge<K, LB>(B, L);
 }
 
 template <int K, bool LB>
-__device__ __forceinline__ void eval_generic(const WarpBuf &B, int n, float qx, float qy, float qz, const Dom &D,
+__device__ __forceinline__ void eval_generic(WarpBuf<K> &B, int n, float qx, float qy, float qz, const Dom &D,
                                              Lane<K, LB> &L) {
   for (int j = 0; j < n; ++j) {
     const float d2 = canon_d2_per(qx, qy, qz, B.x[j], B.y[j], B.z[j], D);  // NaN padding -> NaN
-    cand<K, LB>(L, d2, B.g[j]);
+    append_chk<K, LB>(B, L, d2, B.g[j]);
   }
+  merge<K, LB>(B, L);
 }
 
+struct LeafPK {
+  const float4 *spts;        // source points, z order (type-separated, P:L279)
+  const int32_t *sbeg;       // [nleaf+1] first source of each leaf
+  const float4 *qpts;        // query points, z order
+  const int32_t *qbeg;       // [nleaf+1] first query of each leaf
+  const int32_t *qin;        // [nq] input row of each query
+  const CE *leaf_ce;         // [nleaf]
+  const int32_t *par_leaf;   // [npar+1] first leaf of each receiving parent
+  const CE *par_ce;          // [npar] or nullptr
+  const int64_t *ispl;       // parent-level interaction list
+  const int32_t *isrc;
+  const float *rlow;
+  const float *rmax2;        // [npar] or nullptr (= +inf)
+  const int32_t *item_par;   // [nitems] receiving parent of each 32-query work item
+  const int32_t *item_q0;    // [nitems] first query (sorted position) of the item
+  int64_t nitems;
+  float Lmax;  // periodic: largest box length (margin scale); open: 0
+  int k;       // neighbours found by this pass (<= K)
+  int col0;    // first output column of this pass (k > k_max chunking)
+  int ldo;     // output row stride (total k)
+  int order;
+  int early;
+  int sorted;
+  int32_t *out_idx;
+  float *out_d2;
+  int32_t *out_row_gidx;
+  unsigned long long *stats;  // [0] distance evaluations, [1] top-k insertions (or nullptr)
+};
+
 // Visit the child leaves [la, lb) of one source node, skipping [xa, xb): one lane tests one
-// leaf (exact box bound vs the warp's current max k-th distance), then every lane tests its own
-// query against each surviving leaf (skip unless some lane needs it); survivors are staged in
-// batches of one periodic shift class and evaluated.
+// leaf against the warp's query box (bound vs the warp's current max k-th value), then every
+// lane tests its own query against each surviving leaf (skip unless some lane needs it);
+// survivors are staged in batches of one periodic shift class and evaluated.
 template <int K, bool LB, bool PER>
-__device__ __forceinline__ void visit_leaves(const LeafPK &a, const Dom &D, WarpBuf &B, const NodeBox &wbox, float wmax,
+__device__ __forceinline__ void visit_leaves(const LeafPK &a, const Dom &D, WarpBuf<K> &B, const CE &wb, float wmax,
                                              int la, int lb, int xa, int xb, float qx, float qy, float qz, bool act,
                                              Lane<K, LB> &L, unsigned long long &nev) {
   const int lane = threadIdx.x & 31;
   for (int l0 = la; l0 < lb; l0 += 32) {
     const int l = l0 + lane;
     bool pass = false;
-    int cls = 0;
+    int cls = 0, s0 = 0, s1 = 0;
+    float cx = 0.f, cy = 0.f, cz = 0.f, ex = 0.f, ey = 0.f, ez = 0.f;
     if (l < lb && (l < xa || l >= xb)) {
-      const NodeBox lbx = a.leaf_box[l];
-      pass = box_dlow2(wbox, lbx, D) <= wmax;
-      if (PER && pass) {
-        float shd;
-        cls |= shift_class(wbox.lo.x, wbox.hi.x, lbx.lo.x, lbx.hi.x, D.L[0], D.h[0], shd) << 0;
-        cls |= shift_class(wbox.lo.y, wbox.hi.y, lbx.lo.y, lbx.hi.y, D.L[1], D.h[1], shd) << 2;
-        cls |= shift_class(wbox.lo.z, wbox.hi.z, lbx.lo.z, lbx.hi.z, D.L[2], D.h[2], shd) << 4;
+      const CE lc = a.leaf_ce[l];
+      cx = lc.c.x;
+      cy = lc.c.y;
+      cz = lc.c.z;
+      ex = lc.e.x;
+      ey = lc.e.y;
+      ez = lc.e.z;
+      const float dcx = __fsub_rn(wb.c.x, cx), dcy = __fsub_rn(wb.c.y, cy), dcz = __fsub_rn(wb.c.z, cz);
+      const float Ex = __fadd_ru(wb.e.x, ex), Ey = __fadd_ru(wb.e.y, ey), Ez = __fadd_ru(wb.e.z, ez);
+      pass = dlow2_ce<PER>(dcx, dcy, dcz, Ex, Ey, Ez, D) <= wmax;
+      if (PER && pass)
+        cls = ce_class(dcx, Ex, D.h[0]) | (ce_class(dcy, Ey, D.h[1]) << 2) | (ce_class(dcz, Ez, D.h[2]) << 4);
+      if (pass) {
+        s0 = a.sbeg[l];
+        s1 = a.sbeg[l + 1];
       }
     }
     unsigned bal = __ballot_sync(0xffffffffu, pass);
     while (bal) {
       // batch consecutive surviving leaves of one shift class into the warp buffer
-      const int first = __ffs(bal) - 1;
-      const int c0 = __shfl_sync(0xffffffffu, cls, first);
+      const int c0 = __shfl_sync(0xffffffffu, cls, __ffs(bal) - 1);
       int n = 0;
       while (bal) {
         const int src = __ffs(bal) - 1;
         if (__shfl_sync(0xffffffffu, cls, src) != c0) break;
-        // per-lane test: does any lane's query reach this leaf within its own k-th distance?
+        // per-lane test: does any lane's query reach this leaf within its own k-th value?
         {
-          const NodeBox lbx = a.leaf_box[l0 + src];
-          const bool need = L.act && pt_box_dlow2(qx, qy, qz, lbx, D) <= L.kth;
-          if (!__any_sync(0xffffffffu, need)) {
+          const float lcx = __shfl_sync(0xffffffffu, cx, src), lcy = __shfl_sync(0xffffffffu, cy, src),
+                      lcz = __shfl_sync(0xffffffffu, cz, src);
+          const float lex = __shfl_sync(0xffffffffu, ex, src), ley = __shfl_sync(0xffffffffu, ey, src),
+                      lez = __shfl_sync(0xffffffffu, ez, src);
+          const float dl = dlow2_ce<PER>(__fsub_rn(qx, lcx), __fsub_rn(qy, lcy), __fsub_rn(qz, lcz), lex, ley, lez, D);
+          if (!__any_sync(0xffffffffu, dl <= L.kth)) {
             bal &= bal - 1;
             continue;
           }
         }
-        const int lp = a.sbeg[l0 + src], m = a.sbeg[l0 + src + 1] - lp;
+        const int lp = __shfl_sync(0xffffffffu, s0, src), m = __shfl_sync(0xffffffffu, s1, src) - lp;
         if (n + ((m + 3) & ~3) > kLCap) break;
         bal &= bal - 1;
         for (int t = lane; t < ((m + 3) & ~3); t += 32) {
@@ -296,12 +396,8 @@ __device__ __forceinline__ void visit_leaves(const LeafPK &a, const Dom &D, Warp
       if (!PER || c0 == 0) {
         eval_block<K, LB, false>(B, n, qx, qy, qz, 0.f, 0.f, 0.f, L);
       } else if (!any_straddle(c0)) {  // no axis straddles: uniform exact shift
-        float s0, s1, s2;
-        const NodeBox lbx = a.leaf_box[l0 + first];
-        shift_class(wbox.lo.x, wbox.hi.x, lbx.lo.x, lbx.hi.x, D.L[0], D.h[0], s0);
-        shift_class(wbox.lo.y, wbox.hi.y, lbx.lo.y, lbx.hi.y, D.L[1], D.h[1], s1);
-        shift_class(wbox.lo.z, wbox.hi.z, lbx.lo.z, lbx.hi.z, D.L[2], D.h[2], s2);
-        eval_block<K, LB, true>(B, n, qx, qy, qz, s0, s1, s2, L);
+        eval_block<K, LB, true>(B, n, qx, qy, qz, class_shift(c0 & 3, D.L[0]), class_shift((c0 >> 2) & 3, D.L[1]),
+                                class_shift((c0 >> 4) & 3, D.L[2]), L);
       } else {
         eval_generic<K, LB>(B, n, qx, qy, qz, D, L);
       }
@@ -314,13 +410,34 @@ __device__ __forceinline__ float warp_max_kth(float kth) {
   return __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(fmaxf(kth, 0.f))));
 }
 
+template <int K>
+__device__ __forceinline__ void bitonic_sort(u64 (&T)[K]) {
+#pragma unroll
+  for (int size = 2; size <= K; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        const int j = i ^ stride;
+        if (j > i) {
+          const bool asc = (i & size) == 0;
+          const u64 x = T[i], y = T[j];
+          const bool sw = asc ? (x > y) : (x < y);
+          T[i] = sw ? y : x;
+          T[j] = sw ? x : y;
+        }
+      }
+    }
+  }
+}
+
 template <int K, bool LB, bool PER>
 __global__ void __launch_bounds__(kLThreads) k_leaf(LeafPK a, Dom D) {
-  __shared__ __align__(16) WarpBuf s_buf[kLWarps];
+  __shared__ __align__(16) WarpBuf<K> s_buf[kLWarps];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t item = (int64_t)blockIdx.x * kLWarps + warp;
   if (item >= a.nitems) return;
-  WarpBuf &B = s_buf[warp];
+  WarpBuf<K> &B = s_buf[warp];
   const int J = a.item_par[item];
   const int LJa = a.par_leaf[J], LJb = a.par_leaf[J + 1];
   const int qhi = a.qbeg[LJb];
@@ -347,24 +464,22 @@ __global__ void __launch_bounds__(kLThreads) k_leaf(LeafPK a, Dom D) {
       bhi[d] = fmaxf(bhi[d], __shfl_xor_sync(0xffffffffu, bhi[d], o));
     }
   }
-  NodeBox wbox;
-  wbox.lo = make_float4(blo[0], blo[1], blo[2], 0.f);
-  wbox.hi = make_float4(bhi[0], bhi[1], bhi[2], 0.f);
+  const CE wb = make_ce(blo[0], blo[1], blo[2], bhi[0], bhi[1], bhi[2], a.Lmax);
 
   const float R0 = a.rmax2 ? a.rmax2[J] : INFINITY;
   Lane<K, LB> L;
   {
-    const u64 sentinel = ((u64)__float_as_uint(R0) << 32) | 0xffffffffull;
 #pragma unroll
-    for (int j = 0; j < K; ++j) L.tk[j] = (j < K - a.k) ? 0ull : sentinel;
-    L.kth = act ? R0 : -1.f;  // inactive lanes never pass a comparison
+    for (int j = 0; j < K; ++j) L.F[j] = (j < K - a.k) ? 0.f : R0;  // K - k placeholders <= any d2
+    L.kth = act ? R0 : -1.f;
     L.lb = 0;
     if (LB && act) {  // continue after the last (d2, index) of the previous pass
       const int64_t o = row * a.ldo + a.col0 - 1;
       L.lb = ((u64)__float_as_uint(a.out_d2[o]) << 32) | (unsigned)(a.out_idx[o] + 1);
     }
     L.ins = 0;
-    L.qn = 0;
+    L.nl = 0;
+    L.nf = 0;
     L.act = act;
   }
   unsigned long long nev = 0;
@@ -381,7 +496,7 @@ __global__ void __launch_bounds__(kLThreads) k_leaf(LeafPK a, Dom D) {
         xb = max(xb, l0 + 32 - __clz(b));
       }
     }
-    visit_leaves<K, LB, PER>(a, D, B, wbox, INFINITY, xa, xb, 0, 0, qx, qy, qz, act, L, nev);
+    visit_leaves<K, LB, PER>(a, D, B, wb, INFINITY, xa, xb, 0, 0, qx, qy, qz, act, L, nev);
   }
   const int64_t eb = a.ispl[J], ee = a.ispl[J + 1];
   for (int64_t e = eb; e < ee; ++e) {
@@ -391,10 +506,18 @@ __global__ void __launch_bounds__(kLThreads) k_leaf(LeafPK a, Dom D) {
       if (a.sorted) break;
       continue;
     }
-    if (a.par_box && box_dlow2(wbox, a.par_box[S], D) > wmax) continue;
-    visit_leaves<K, LB, PER>(a, D, B, wbox, wmax, a.par_leaf[S], a.par_leaf[S + 1], S == J ? xa : 0, S == J ? xb : 0, qx,
-                         qy, qz, act, L, nev);
+    if (a.par_ce) {
+      const CE pc = a.par_ce[S];
+      const float d = dlow2_ce<PER>(__fsub_rn(wb.c.x, pc.c.x), __fsub_rn(wb.c.y, pc.c.y), __fsub_rn(wb.c.z, pc.c.z),
+                                    __fadd_ru(wb.e.x, pc.e.x), __fadd_ru(wb.e.y, pc.e.y), __fadd_ru(wb.e.z, pc.e.z), D);
+      if (d > wmax) continue;
+    }
+    visit_leaves<K, LB, PER>(a, D, B, wb, wmax, a.par_leaf[S], a.par_leaf[S + 1], S == J ? xa : 0, S == J ? xb : 0, qx,
+                             qy, qz, act, L, nev);
   }
+  // the row: the k smallest keys of the log (all entries <= the final k-th value)
+  compact<K, LB>(B, L);
+  if (L.nl > a.k) L.nl = drop_largest<K>(B, L.nl, a.k);
   if (a.stats) {
     unsigned long long tot = nev, ins = L.ins;
 #pragma unroll
@@ -408,13 +531,17 @@ __global__ void __launch_bounds__(kLThreads) k_leaf(LeafPK a, Dom D) {
     }
   }
   if (act) {
+    u64 T[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) T[j] = j < L.nl ? B.log[j][lane] : ~0ull;
+    bitonic_sort<K>(T);
     int32_t *oi = a.out_idx + row * a.ldo + a.col0;
     float *od = a.out_d2 + row * a.ldo + a.col0;
 #pragma unroll
     for (int j = 0; j < K; ++j) {
-      if (j >= K - a.k) {
-        oi[j - (K - a.k)] = (int32_t)((unsigned)(L.tk[j] & 0xffffffffu) - 1u);
-        od[j - (K - a.k)] = __uint_as_float((unsigned)(L.tk[j] >> 32));
+      if (j < a.k) {
+        oi[j] = (int32_t)((unsigned)(T[j] & 0xffffffffu) - 1u);
+        od[j] = __uint_as_float((unsigned)(T[j] >> 32));
       }
     }
     if (a.out_row_gidx) a.out_row_gidx[row] = __float_as_int(qw);
@@ -470,6 +597,16 @@ void leaf_to_leaf(const LeafArgs &a, const Dom &D, cudaStream_t st) {
   JZ_CUDA(cudaMallocAsync(&item_q0, (nitems + 1) * sizeof(int32_t), st));
   k_item_fill<<<grid_for(a.npar, 256), 256, 0, st>>>(a.par_leaf, a.qbeg, a.npar, chunk, off, item_par, item_q0);
   JZ_LAUNCH_CHECK();
+  const float Lmax = D.periodic ? fmaxf(fmaxf(D.L[0], D.L[1]), D.L[2]) : 0.f;
+  CE *leaf_ce = nullptr, *par_ce = nullptr;
+  JZ_CUDA(cudaMallocAsync(&leaf_ce, (a.nleaf > 0 ? a.nleaf : 1) * sizeof(CE), st));
+  k_box_ce<<<grid_for(a.nleaf, 256), 256, 0, st>>>(a.leaf_box, a.nleaf, Lmax, leaf_ce);
+  JZ_LAUNCH_CHECK();
+  if (a.par_box) {
+    JZ_CUDA(cudaMallocAsync(&par_ce, a.npar * sizeof(CE), st));
+    k_box_ce<<<grid_for(a.npar, 256), 256, 0, st>>>(a.par_box, a.npar, Lmax, par_ce);
+    JZ_LAUNCH_CHECK();
+  }
 
   LeafPK la;
   la.spts = a.spts;
@@ -477,9 +614,9 @@ void leaf_to_leaf(const LeafArgs &a, const Dom &D, cudaStream_t st) {
   la.qpts = a.qpts;
   la.qbeg = a.qbeg;
   la.qin = a.qin;
-  la.leaf_box = a.leaf_box;
+  la.leaf_ce = leaf_ce;
   la.par_leaf = a.par_leaf;
-  la.par_box = a.par_box;
+  la.par_ce = par_ce;
   la.ispl = a.il->ispl;
   la.isrc = a.il->isrc;
   la.rlow = a.il->rlow;
@@ -487,6 +624,7 @@ void leaf_to_leaf(const LeafArgs &a, const Dom &D, cudaStream_t st) {
   la.item_par = item_par;
   la.item_q0 = item_q0;
   la.nitems = nitems;
+  la.Lmax = Lmax;
   la.ldo = a.k;
   la.order = a.order;
   la.early = !(a.flags & JZ_FLAG_NO_EARLY_EXIT);
@@ -512,6 +650,8 @@ void leaf_to_leaf(const LeafArgs &a, const Dom &D, cudaStream_t st) {
   JZ_CUDA(cudaFreeAsync(off, st));
   JZ_CUDA(cudaFreeAsync(item_par, st));
   JZ_CUDA(cudaFreeAsync(item_q0, st));
+  JZ_CUDA(cudaFreeAsync(leaf_ce, st));
+  if (par_ce) JZ_CUDA(cudaFreeAsync(par_ce, st));
 }
 
 }  // namespace jz
