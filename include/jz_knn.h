@@ -158,9 +158,9 @@ JZ_API int jz_knn_stage_times(const jz_knn_index *ix, float out_ms[6], int64_t *
 JZ_API void jz_set_timing(int on);
 
 /* Counters of the last query (host out[9]): [0] distance evaluations, [1] top-k insertions,
- * [2] number of leaves, [3] number of tree planes, LeafToLeaf walk: [4] interaction entries
- * visited, [5] leaves passing the warp box test, [6] leaves staged, [7] insertion rounds,
- * [8] 32-query work items. */
+ * [2] number of leaves, [3] number of tree planes, LeafToLeaf: [4] candidate-log appends,
+ * [5] top-k merge rounds (per warp), [6] log compactions (per warp), [7] leaves staged (per
+ * warp), [8] 32-query work items. */
 JZ_API int jz_knn_stats(const jz_knn_index *ix, int64_t out[9]);
 
 /* Number of kernels this library has launched in the process so far. */

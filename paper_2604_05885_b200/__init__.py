@@ -98,7 +98,7 @@ class KnnIndex:
         st = (ctypes.c_int64 * 9)()
         B.check(self._lib.jz_knn_stats(self._h, st))
         d["inserts"], d["leaves"], d["planes"] = st[1], st[2], st[3]
-        d["walk"] = {"entries": st[4], "leaves_warp": st[5], "leaves_staged": st[6], "rounds": st[7], "items": st[8]}
+        d["walk"] = {"appends": st[4], "merge_rounds": st[5], "compactions": st[6], "leaves_staged": st[7], "items": st[8]}
         return d
 
     # ---- introspection (tests)

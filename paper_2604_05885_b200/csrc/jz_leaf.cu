@@ -33,11 +33,27 @@ namespace jz {
 
 constexpr int kLWarps = 2;
 constexpr int kLThreads = kLWarps * 32;
-constexpr int kLCap = 256;  // staged source points per warp (4 KB SoA)
+#ifndef JZ_LCAP
+#define JZ_LCAP 256
+#endif
+#ifndef JZ_MINB
+#define JZ_MINB 9  // 9 CTAs x 2 warps per SM: 112 registers (smem allows 9 CTAs at K = 16)
+#endif
+constexpr int kLCap = JZ_LCAP;  // staged source points per warp (4 KB SoA)
+
+#ifndef JZ_LOGX
+#define JZ_LOGX 16
+#endif
+#ifndef JZ_HALFGATE
+#define JZ_HALFGATE 1
+#endif
+#ifndef JZ_MERGE_EACH
+#define JZ_MERGE_EACH 0
+#endif
 
 template <int K>
 struct LogCap {
-  static constexpr int C = K + 16;  // log entries per lane
+  static constexpr int C = K + JZ_LOGX;  // log entries per lane
 };
 
 typedef unsigned long long u64;
@@ -139,13 +155,39 @@ __global__ void k_box_ce(const NodeBox *__restrict__ box, int64_t n, float Lmax,
 }
 
 // ---------------------------------------------------------------- top-k state
+// insert value d into the sorted list F, dropping the largest (identity when d >= F[K-1]):
+// F'[j] = max(F[j-1], min(F[j], d)), F'[0] = min(F[0], d) -- every slot independent (depth 2,
+// no serial chain). Warp-converged: the lower half runs only when some lane's d lands there.
+#ifndef JZ_PAR_INSERT
+#define JZ_PAR_INSERT 1
+#endif
 template <int K>
 __device__ __forceinline__ void bubble(float (&F)[K], float d) {
+  constexpr int J0 = JZ_HALFGATE ? K / 2 : 0;
+  if (JZ_PAR_INSERT) {
 #pragma unroll
-  for (int j = 0; j < K; ++j) {
-    const float lo = fminf(F[j], d);
-    d = fmaxf(F[j], d);
-    F[j] = lo;
+    for (int j = K - 1; j >= J0 && j > 0; --j) F[j] = fmaxf(F[j - 1], fminf(F[j], d));
+    if (J0 > 0 && __any_sync(0xffffffffu, d < F[J0 > 0 ? J0 - 1 : 0])) {
+#pragma unroll
+      for (int j = J0 - 1; j > 0; --j) F[j] = fmaxf(F[j - 1], fminf(F[j], d));
+      F[0] = fminf(F[0], d);
+    }
+    if (J0 == 0) F[0] = fminf(F[0], d);
+  } else {
+    if (J0 > 0 && __any_sync(0xffffffffu, d < F[J0 > 0 ? J0 - 1 : 0])) {
+#pragma unroll
+      for (int j = 0; j < J0; ++j) {
+        const float lo = fminf(F[j], d);
+        d = fmaxf(F[j], d);
+        F[j] = lo;
+      }
+    }
+#pragma unroll
+    for (int j = J0; j < K; ++j) {
+      const float lo = fminf(F[j], d);
+      d = fmaxf(F[j], d);
+      F[j] = lo;
+    }
   }
 }
 
@@ -164,6 +206,10 @@ struct Lane {
   int nl;      // log entries
   int nf;      // log entries already merged into F
   unsigned ins;
+  unsigned app;   // log appends (lane)
+  unsigned rnd;   // merge rounds (warp-uniform)
+  unsigned cmp;   // compactions (warp-uniform)
+  unsigned stg;   // staged leaves (warp-uniform)
   bool act;
 };
 
@@ -171,15 +217,15 @@ struct Lane {
 template <int K, bool LB>
 __device__ __forceinline__ void merge(WarpBuf<K> &B, Lane<K, LB> &L) {
   const int lane = threadIdx.x & 31;
-  const int r0 = (int)__reduce_min_sync(0xffffffffu, (unsigned)L.nf);
-  const int r1 = (int)__reduce_max_sync(0xffffffffu, (unsigned)L.nl);
-  for (int r = r0; r < r1; ++r) {
+  const int nr = (int)__reduce_max_sync(0xffffffffu, (unsigned)(L.nl - L.nf));
+  L.rnd += nr;
+  for (int i = 0; i < nr; ++i) {
+    const int r = L.nf + i;
     float d = INFINITY;
-    if (r >= L.nf && r < L.nl) d = __uint_as_float((unsigned)(B.log[r][lane] >> 32));
-    if (d < L.F[K - 1]) {
-      bubble<K>(L.F, d);
-      ++L.ins;
-    }
+    if (r < L.nl) d = __uint_as_float((unsigned)(B.log[r][lane] >> 32));
+    const bool in = d < L.F[K - 1];
+    if (__any_sync(0xffffffffu, in)) bubble<K>(L.F, d);
+    L.ins += in;
   }
   L.nf = L.nl;
   L.kth = L.act ? L.F[K - 1] : -1.f;
@@ -210,6 +256,7 @@ template <int K, bool LB>
 __device__ __forceinline__ void compact(WarpBuf<K> &B, Lane<K, LB> &L) {
   constexpr int C = LogCap<K>::C;
   const int lane = threadIdx.x & 31;
+  ++L.cmp;
   merge<K, LB>(B, L);
   const unsigned kb = __float_as_uint(L.kth);
   const int r1 = (int)__reduce_max_sync(0xffffffffu, (unsigned)L.nl);
@@ -234,6 +281,7 @@ __device__ __forceinline__ void append(WarpBuf<K> &B, Lane<K, LB> &L, float d2, 
     if (!LB || key > L.lb) {
       B.log[L.nl][threadIdx.x & 31] = key;
       ++L.nl;
+      ++L.app;
     }
   }
 }
@@ -246,9 +294,11 @@ __device__ __forceinline__ void append_chk(WarpBuf<K> &B, Lane<K, LB> &L, float 
 
 // ---------------------------------------------------------------- distance evaluation
 // staged sources [0, n) (n multiple of 4, NaN padded) against the lane's query
-template <int K, bool LB, bool SHIFT>
+// MASK: skip the lane's own window of K staged sources starting at staged index wl (those are
+// already in the list, see window_init)
+template <int K, bool LB, bool SHIFT, bool MASK = false>
 __device__ __forceinline__ void eval_block(WarpBuf<K> &B, int n, float qx, float qy, float qz, float shx, float shy,
-                                           float shz, Lane<K, LB> &L) {
+                                           float shz, Lane<K, LB> &L, int wl = 0) {
   constexpr int C = LogCap<K>::C;
   const u64 QX = pk(qx, qx), QY = pk(qy, qy), QZ = pk(qz, qz);
   const u64 SX = pk(shx, shx), SY = pk(shy, shy), SZ = pk(shz, shz);
@@ -272,6 +322,14 @@ __device__ __forceinline__ void eval_block(WarpBuf<K> &B, int n, float qx, float
     float a0, a1, a2, a3;
     upk(d0, a0, a1);
     upk(d1, a2, a3);
+    if (MASK) {
+      const unsigned u = (unsigned)(j - wl);
+      const float nan = __int_as_float(0x7fc00000);
+      if (u < (unsigned)K) a0 = nan;
+      if (u + 1u < (unsigned)K) a1 = nan;
+      if (u + 2u < (unsigned)K) a2 = nan;
+      if (u + 3u < (unsigned)K) a3 = nan;
+    }
     const float m = fminf(fminf(a0, a1), fminf(a2, a3));  // NaN padding is ignored by min
     if (__any_sync(0xffffffffu, m <= L.kth)) {
       const int4 G = *reinterpret_cast<const int4 *>(&B.g[j]);
@@ -280,16 +338,18 @@ __device__ __forceinline__ void eval_block(WarpBuf<K> &B, int n, float qx, float
       append<K, LB>(B, L, a2, G.z);
       append<K, LB>(B, L, a3, G.w);
       if (__any_sync(0xffffffffu, L.nl > C - 4)) compact<K, LB>(B, L);
+      else if (JZ_MERGE_EACH) merge<K, LB>(B, L);
     }
   }
   merge<K, LB>(B, L);
 }
 
-template <int K, bool LB>
+template <int K, bool LB, bool MASK = false>
 __device__ __forceinline__ void eval_generic(WarpBuf<K> &B, int n, float qx, float qy, float qz, const Dom &D,
-                                             Lane<K, LB> &L) {
+                                             Lane<K, LB> &L, int wl = 0) {
   for (int j = 0; j < n; ++j) {
-    const float d2 = canon_d2_per(qx, qy, qz, B.x[j], B.y[j], B.z[j], D);  // NaN padding -> NaN
+    float d2 = canon_d2_per(qx, qy, qz, B.x[j], B.y[j], B.z[j], D);  // NaN padding -> NaN
+    if (MASK && (unsigned)(j - wl) < (unsigned)K) d2 = __int_as_float(0x7fc00000);
     append_chk<K, LB>(B, L, d2, B.g[j]);
   }
   merge<K, LB>(B, L);
@@ -321,7 +381,8 @@ struct LeafPK {
   int32_t *out_idx;
   float *out_d2;
   int32_t *out_row_gidx;
-  unsigned long long *stats;  // [0] distance evaluations, [1] top-k insertions (or nullptr)
+  int self;    // queries == sources (self-query): enables the z-window initialisation
+  unsigned long long *stats;  // counters (jz_knn_stats) or nullptr
 };
 
 // Visit the child leaves [la, lb) of one source node, skipping [xa, xb): one lane tests one
@@ -389,6 +450,7 @@ __device__ __forceinline__ void visit_leaves(const LeafPK &a, const Dom &D, Warp
           B.g[n + t] = __float_as_int(p.w);
         }
         nev += act ? (unsigned)m : 0u;
+        ++L.stg;
         n += (m + 3) & ~3;
       }
       __syncwarp();
@@ -431,8 +493,85 @@ __device__ __forceinline__ void bitonic_sort(u64 (&T)[K]) {
   }
 }
 
+template <int K>
+__device__ __forceinline__ void bitonic_sort_f(float (&T)[K]) {
+#pragma unroll
+  for (int size = 2; size <= K; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        const int j = i ^ stride;
+        if (j > i) {
+          const float lo = fminf(T[i], T[j]), hi = fmaxf(T[i], T[j]);
+          const bool asc = (i & size) == 0;
+          T[i] = asc ? lo : hi;
+          T[j] = asc ? hi : lo;
+        }
+      }
+    }
+  }
+}
+
+// z-window initialisation (self-query): the K sources at sorted positions [wpos, wpos + K)
+// around the lane's own query are evaluated first; their keys start the log and their sorted
+// values the list, so the k-th value is already close before the own leaves are scanned
+// (z-order neighbours are mostly spatial neighbours, P:L69 / Fig. 2).
 template <int K, bool LB, bool PER>
-__global__ void __launch_bounds__(kLThreads) k_leaf(LeafPK a, Dom D) {
+__device__ __forceinline__ void window_init(const LeafPK &a, const Dom &D, WarpBuf<K> &B, int wpos, float qx,
+                                            float qy, float qz, bool act, Lane<K, LB> &L) {
+  const int lane = threadIdx.x & 31;
+  float W[K];
+#pragma unroll
+  for (int o = 0; o < K; ++o) {
+    W[o] = INFINITY;
+    if (act) {
+      const float4 p = a.spts[wpos + o];
+      const float d = PER ? canon_d2_per(qx, qy, qz, p.x, p.y, p.z, D) : canon_d2_open(qx, qy, qz, p.x, p.y, p.z);
+      W[o] = d;
+      B.log[o][lane] = ((u64)__float_as_uint(d) << 32) | (unsigned)(__float_as_int(p.w) + 1);
+    }
+  }
+  bitonic_sort_f<K>(W);
+#pragma unroll
+  for (int j = 0; j < K; ++j) L.F[j] = W[j];
+  L.nl = L.nf = act ? K : 0;
+  L.app += act ? K : 0;
+  L.kth = act ? L.F[K - 1] : -1.f;
+}
+
+// pre-pass over the warp's own sources [s0, s1) (the sources of the leaves holding its
+// queries; contiguous in z order): staged without per-leaf alignment, lanes skip their
+// window (already in the list); cls_all = OR of the own leaves' shift classes.
+template <int K, bool LB, bool PER>
+__device__ __forceinline__ void own_pass(const LeafPK &a, const Dom &D, WarpBuf<K> &B, int s0, int s1, int cls_all,
+                                         int wpos, float qx, float qy, float qz, bool act, Lane<K, LB> &L,
+                                         unsigned long long &nev) {
+  const int lane = threadIdx.x & 31;
+  for (int b0 = s0; b0 < s1; b0 += kLCap) {
+    const int m = min(kLCap, s1 - b0), mp = (m + 3) & ~3;
+    for (int t = lane; t < mp; t += 32) {
+      float4 p = make_float4(__int_as_float(0x7fc00000), __int_as_float(0x7fc00000), __int_as_float(0x7fc00000), 0.f);
+      if (t < m) p = a.spts[b0 + t];
+      B.x[t] = p.x;
+      B.y[t] = p.y;
+      B.z[t] = p.z;
+      B.g[t] = __float_as_int(p.w);
+    }
+    nev += act ? (unsigned)m : 0u;
+    __syncwarp();
+    const int wl = wpos - b0;
+    if (!PER || cls_all == 0) {
+      eval_block<K, LB, false, true>(B, mp, qx, qy, qz, 0.f, 0.f, 0.f, L, wl);
+    } else {
+      eval_generic<K, LB, true>(B, mp, qx, qy, qz, D, L, wl);
+    }
+    __syncwarp();
+  }
+}
+
+template <int K, bool LB, bool PER>
+__global__ void __launch_bounds__(kLThreads, JZ_MINB) k_leaf(LeafPK a, Dom D) {
   __shared__ __align__(16) WarpBuf<K> s_buf[kLWarps];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t item = (int64_t)blockIdx.x * kLWarps + warp;
@@ -478,6 +617,7 @@ __global__ void __launch_bounds__(kLThreads) k_leaf(LeafPK a, Dom D) {
       L.lb = ((u64)__float_as_uint(a.out_d2[o]) << 32) | (unsigned)(a.out_idx[o] + 1);
     }
     L.ins = 0;
+    L.app = L.rnd = L.cmp = L.stg = 0;
     L.nl = 0;
     L.nf = 0;
     L.act = act;
@@ -496,7 +636,24 @@ __global__ void __launch_bounds__(kLThreads) k_leaf(LeafPK a, Dom D) {
         xb = max(xb, l0 + 32 - __clz(b));
       }
     }
-    visit_leaves<K, LB, PER>(a, D, B, wb, INFINITY, xa, xb, 0, 0, qx, qy, qz, act, L, nev);
+    const int s0o = a.sbeg[xa], s1o = a.sbeg[xb];
+    int wpos = -0x40000000;  // far from every staged index: no window
+    if (!LB && a.self && a.k == K && s1o - s0o >= K) {
+      if (act) wpos = min(max(qi - K / 2, s0o), s1o - K);
+      window_init<K, LB, PER>(a, D, B, wpos, qx, qy, qz, act, L);
+    }
+    int cls_all = 0;
+    if (PER) {
+      for (int l = xa + lane; l < xb; l += 32) {
+        const CE lc = a.leaf_ce[l];
+        const float dcx = __fsub_rn(wb.c.x, lc.c.x), dcy = __fsub_rn(wb.c.y, lc.c.y), dcz = __fsub_rn(wb.c.z, lc.c.z);
+        cls_all |= ce_class(dcx, __fadd_ru(wb.e.x, lc.e.x), D.h[0]) | ce_class(dcy, __fadd_ru(wb.e.y, lc.e.y), D.h[1]) |
+                   ce_class(dcz, __fadd_ru(wb.e.z, lc.e.z), D.h[2]);
+      }
+      cls_all = __reduce_or_sync(0xffffffffu, cls_all);
+    }
+    L.stg += xb - xa;
+    own_pass<K, LB, PER>(a, D, B, s0o, s1o, cls_all, wpos, qx, qy, qz, act, L, nev);
   }
   const int64_t eb = a.ispl[J], ee = a.ispl[J + 1];
   for (int64_t e = eb; e < ee; ++e) {
@@ -519,15 +676,21 @@ __global__ void __launch_bounds__(kLThreads) k_leaf(LeafPK a, Dom D) {
   compact<K, LB>(B, L);
   if (L.nl > a.k) L.nl = drop_largest<K>(B, L.nl, a.k);
   if (a.stats) {
-    unsigned long long tot = nev, ins = L.ins;
+    unsigned long long tot = nev, ins = L.ins, app = L.app;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       tot += __shfl_xor_sync(0xffffffffu, tot, o);
       ins += __shfl_xor_sync(0xffffffffu, ins, o);
+      app += __shfl_xor_sync(0xffffffffu, app, o);
     }
     if (lane == 0) {
       atomicAdd(&a.stats[0], tot);
       atomicAdd(&a.stats[1], ins);
+      atomicAdd(&a.stats[2], app);
+      atomicAdd(&a.stats[3], (unsigned long long)L.rnd);
+      atomicAdd(&a.stats[4], (unsigned long long)L.cmp);
+      atomicAdd(&a.stats[5], (unsigned long long)L.stg);
+      atomicAdd(&a.stats[6], 1ull);
     }
   }
   if (act) {
@@ -633,6 +796,7 @@ void leaf_to_leaf(const LeafArgs &a, const Dom &D, cudaStream_t st) {
   la.out_d2 = a.out_d2;
   la.out_row_gidx = a.out_row_gidx;
   la.stats = a.evals;
+  la.self = a.spts == a.qpts;
   if (nitems > 0) {
     const unsigned blocks = (unsigned)ceil_div(nitems, kLWarps);
     // k > k_max: ceil(k / k_max) passes over the same interaction list (built for R_max(k));

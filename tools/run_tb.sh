@@ -5,5 +5,5 @@ timeout 500 python bench.py --steps 3 --warmup 2 --no-e2e --no-cpu-baseline > gp
 python - <<'PY' $1
 import json,sys
 l=open(f"gpurun_out/bench_{sys.argv[1]}.log").read().strip().splitlines()[-1]
-d=json.loads(l); print("value %.3e ms %.1f"%(d["value"],d["ms_per_step"]), {k:round(v,2) for k,v in d["stages_ms"].items()}, "evals/q %.0f"%d["evals_per_query"], "frac %.3f"%d["roofline"]["frac"])
+d=json.loads(l); print("value %.3e ms %.1f"%(d["value"],d["ms_per_step"]), {k:round(v,2) for k,v in d["stages_ms"].items()}, "evals/q %.0f"%d["evals_per_query"], "frac %.3f"%d["roofline"]["frac"], "ins/q %.1f"%d["inserts_per_query"], {k:round(v,1) for k,v in d["walk_per_item"].items()})
 PY
