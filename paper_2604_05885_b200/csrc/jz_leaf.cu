@@ -193,9 +193,10 @@ __device__ __forceinline__ void bubble(float (&F)[K], float d) {
 
 template <int K>
 struct WarpBuf {
-  float x[kLCap], y[kLCap], z[kLCap];
-  int g[kLCap];
-  u64 log[LogCap<K>::C][32];  // lane-minor: conflict-free
+  float x[kLCap + 8], y[kLCap + 8], z[kLCap + 8];  // + 8: padding to a multiple of 8
+  int g[kLCap + 8];
+  unsigned ld[LogCap<K>::C][32];  // log: d2 bits (lane-minor: conflict-free)
+  unsigned lg[LogCap<K>::C][32];  // log: gidx + 1
 };
 
 template <int K, bool LB>
@@ -219,10 +220,12 @@ __device__ __forceinline__ void merge(WarpBuf<K> &B, Lane<K, LB> &L) {
   const int lane = threadIdx.x & 31;
   const int nr = (int)__reduce_max_sync(0xffffffffu, (unsigned)(L.nl - L.nf));
   L.rnd += nr;
+  unsigned nx = L.nf < L.nl ? B.ld[L.nf][lane] : 0x7f800000u;
+#pragma unroll 1
   for (int i = 0; i < nr; ++i) {
     const int r = L.nf + i;
-    float d = INFINITY;
-    if (r < L.nl) d = __uint_as_float((unsigned)(B.log[r][lane] >> 32));
+    const float d = __uint_as_float(nx);
+    nx = r + 1 < L.nl ? B.ld[r + 1][lane] : 0x7f800000u;  // prefetch the next round's entry
     const bool in = d < L.F[K - 1];
     if (__any_sync(0xffffffffu, in)) bubble<K>(L.F, d);
     L.ins += in;
@@ -240,13 +243,14 @@ __device__ __noinline__ int drop_largest(WarpBuf<K> &B, int nl, int keep) {
     int im = 0;
     u64 mk = 0;
     for (int r = 0; r < nl; ++r) {
-      const u64 e = B.log[r][lane];
+      const u64 e = ((u64)B.ld[r][lane] << 32) | B.lg[r][lane];
       if (e > mk) {
         mk = e;
         im = r;
       }
     }
-    B.log[im][lane] = B.log[nl - 1][lane];
+    B.ld[im][lane] = B.ld[nl - 1][lane];
+    B.lg[im][lane] = B.lg[nl - 1][lane];
     --nl;
   }
   return nl;
@@ -261,11 +265,23 @@ __device__ __forceinline__ void compact(WarpBuf<K> &B, Lane<K, LB> &L) {
   const unsigned kb = __float_as_uint(L.kth);
   const int r1 = (int)__reduce_max_sync(0xffffffffu, (unsigned)L.nl);
   int j = 0;
-  for (int r = 0; r < r1; ++r) {
-    if (r < L.nl) {
-      const u64 e = B.log[r][lane];
-      if ((unsigned)(e >> 32) <= kb) {
-        B.log[j][lane] = e;
+#pragma unroll 1
+  for (int r = 0; r < r1; r += 4) {  // 4 independent loads per step
+    unsigned d[4], g[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      d[u] = 0xffffffffu;
+      g[u] = 0;
+      if (r + u < L.nl) {
+        d[u] = B.ld[r + u][lane];
+        g[u] = B.lg[r + u][lane];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (d[u] <= kb) {  // 0xffffffff (no entry) never passes: kb <= 0x7f800000 or inactive
+        B.ld[j][lane] = d[u];
+        B.lg[j][lane] = g[u];
         ++j;
       }
     }
@@ -279,7 +295,8 @@ __device__ __forceinline__ void append(WarpBuf<K> &B, Lane<K, LB> &L, float d2, 
   if (d2 <= L.kth) {
     const u64 key = ((u64)__float_as_uint(d2) << 32) | (unsigned)(g + 1);
     if (!LB || key > L.lb) {
-      B.log[L.nl][threadIdx.x & 31] = key;
+      B.ld[L.nl][threadIdx.x & 31] = __float_as_uint(d2);
+      B.lg[L.nl][threadIdx.x & 31] = (unsigned)(g + 1);
       ++L.nl;
       ++L.app;
     }
@@ -289,67 +306,116 @@ __device__ __forceinline__ void append(WarpBuf<K> &B, Lane<K, LB> &L, float d2, 
 template <int K, bool LB>
 __device__ __forceinline__ void append_chk(WarpBuf<K> &B, Lane<K, LB> &L, float d2, int g) {
   append<K, LB>(B, L, d2, g);
-  if (__any_sync(0xffffffffu, L.nl > LogCap<K>::C - 4)) compact<K, LB>(B, L);  // keep nl <= C - 4 between groups
+  if (__any_sync(0xffffffffu, L.nl > LogCap<K>::C - 8)) compact<K, LB>(B, L);  // keep nl <= C - 8 between steps
 }
 
 // ---------------------------------------------------------------- distance evaluation
-// staged sources [0, n) (n multiple of 4, NaN padded) against the lane's query
-// MASK: skip the lane's own window of K staged sources starting at staged index wl (those are
-// already in the list, see window_init)
-template <int K, bool LB, bool SHIFT, bool MASK = false>
-__device__ __forceinline__ void eval_block(WarpBuf<K> &B, int n, float qx, float qy, float qz, float shx, float shy,
-                                           float shz, Lane<K, LB> &L, int wl = 0) {
+// d2 of 4 staged sources [j, j+4) against the lane's query (packed: 2 sources per instruction)
+__device__ __forceinline__ void d2x4(const float *bx, const float *by, const float *bz, int j, u64 QX, u64 QY, u64 QZ,
+                                     bool shift, u64 SX, u64 SY, u64 SZ, float &a0, float &a1, float &a2, float &a3) {
+  const float4 X = *reinterpret_cast<const float4 *>(&bx[j]);
+  const float4 Y = *reinterpret_cast<const float4 *>(&by[j]);
+  const float4 Z = *reinterpret_cast<const float4 *>(&bz[j]);
+  u64 tx0 = sub2(QX, pk(X.x, X.y)), tx1 = sub2(QX, pk(X.z, X.w));
+  u64 ty0 = sub2(QY, pk(Y.x, Y.y)), ty1 = sub2(QY, pk(Y.z, Y.w));
+  u64 tz0 = sub2(QZ, pk(Z.x, Z.y)), tz1 = sub2(QZ, pk(Z.z, Z.w));
+  if (shift) {  // warp-uniform
+    tx0 = add2(tx0, SX);
+    tx1 = add2(tx1, SX);
+    ty0 = add2(ty0, SY);
+    ty1 = add2(ty1, SY);
+    tz0 = add2(tz0, SZ);
+    tz1 = add2(tz1, SZ);
+  }
+  const u64 d0 = fma2(tz0, tz0, fma2(ty0, ty0, mul2(tx0, tx0)));
+  const u64 d1 = fma2(tz1, tz1, fma2(ty1, ty1, mul2(tx1, tx1)));
+  upk(d0, a0, a1);
+  upk(d1, a2, a3);
+}
+
+template <int MW>
+__device__ __forceinline__ void mask4(int j, int wl, float &a0, float &a1, float &a2, float &a3) {
+  if constexpr (MW > 0) {
+    const unsigned u = (unsigned)(j - wl);
+    const float nan = __int_as_float(0x7fc00000);
+    if (u < (unsigned)MW) a0 = nan;
+    if (u + 1u < (unsigned)MW) a1 = nan;
+    if (u + 2u < (unsigned)MW) a2 = nan;
+    if (u + 3u < (unsigned)MW) a3 = nan;
+  }
+}
+
+// staged sources [0, n) (n multiple of 8, NaN padded) against the lane's query; 8 sources per
+// step (two independent packed chains) and one vote. shift: every pair wraps by (shx, shy, shz)
+// (exact, warp-uniform); mw > 0: skip the lane's own window of mw staged sources starting at
+// staged index wl (already in the list, see window_init). One copy of this loop per call site:
+// the flags are runtime (warp-uniform) to keep the hot code small (instruction cache).
+template <int K, bool LB>
+__device__ __forceinline__ void eval_block(WarpBuf<K> &B, int n, float qx, float qy, float qz, bool shift, float shx,
+                                           float shy, float shz, Lane<K, LB> &L, int mw, int wl) {
   constexpr int C = LogCap<K>::C;
   const u64 QX = pk(qx, qx), QY = pk(qy, qy), QZ = pk(qz, qz);
   const u64 SX = pk(shx, shx), SY = pk(shy, shy), SZ = pk(shz, shz);
-  for (int j = 0; j < n; j += 4) {
-    const float4 X = *reinterpret_cast<const float4 *>(&B.x[j]);
-    const float4 Y = *reinterpret_cast<const float4 *>(&B.y[j]);
-    const float4 Z = *reinterpret_cast<const float4 *>(&B.z[j]);
-    u64 tx0 = sub2(QX, pk(X.x, X.y)), tx1 = sub2(QX, pk(X.z, X.w));
-    u64 ty0 = sub2(QY, pk(Y.x, Y.y)), ty1 = sub2(QY, pk(Y.z, Y.w));
-    u64 tz0 = sub2(QZ, pk(Z.x, Z.y)), tz1 = sub2(QZ, pk(Z.z, Z.w));
-    if (SHIFT) {
-      tx0 = add2(tx0, SX);
-      tx1 = add2(tx1, SX);
-      ty0 = add2(ty0, SY);
-      ty1 = add2(ty1, SY);
-      tz0 = add2(tz0, SZ);
-      tz1 = add2(tz1, SZ);
-    }
-    const u64 d0 = fma2(tz0, tz0, fma2(ty0, ty0, mul2(tx0, tx0)));
-    const u64 d1 = fma2(tz1, tz1, fma2(ty1, ty1, mul2(tx1, tx1)));
-    float a0, a1, a2, a3;
-    upk(d0, a0, a1);
-    upk(d1, a2, a3);
-    if (MASK) {
+#pragma unroll 1
+  for (int j = 0; j < n; j += 8) {
+    float a0, a1, a2, a3, b0, b1, b2, b3;
+    d2x4(B.x, B.y, B.z, j, QX, QY, QZ, shift, SX, SY, SZ, a0, a1, a2, a3);
+    d2x4(B.x, B.y, B.z, j + 4, QX, QY, QZ, shift, SX, SY, SZ, b0, b1, b2, b3);
+    if (mw > 0) {
       const unsigned u = (unsigned)(j - wl);
       const float nan = __int_as_float(0x7fc00000);
-      if (u < (unsigned)K) a0 = nan;
-      if (u + 1u < (unsigned)K) a1 = nan;
-      if (u + 2u < (unsigned)K) a2 = nan;
-      if (u + 3u < (unsigned)K) a3 = nan;
+      a0 = u < (unsigned)mw ? nan : a0;
+      a1 = u + 1u < (unsigned)mw ? nan : a1;
+      a2 = u + 2u < (unsigned)mw ? nan : a2;
+      a3 = u + 3u < (unsigned)mw ? nan : a3;
+      b0 = u + 4u < (unsigned)mw ? nan : b0;
+      b1 = u + 5u < (unsigned)mw ? nan : b1;
+      b2 = u + 6u < (unsigned)mw ? nan : b2;
+      b3 = u + 7u < (unsigned)mw ? nan : b3;
     }
-    const float m = fminf(fminf(a0, a1), fminf(a2, a3));  // NaN padding is ignored by min
+    const float m = fminf(fminf(fminf(a0, a1), fminf(a2, a3)), fminf(fminf(b0, b1), fminf(b2, b3)));  // NaN ignored
     if (__any_sync(0xffffffffu, m <= L.kth)) {
       const int4 G = *reinterpret_cast<const int4 *>(&B.g[j]);
+      const int4 H = *reinterpret_cast<const int4 *>(&B.g[j + 4]);
       append<K, LB>(B, L, a0, G.x);
       append<K, LB>(B, L, a1, G.y);
       append<K, LB>(B, L, a2, G.z);
       append<K, LB>(B, L, a3, G.w);
-      if (__any_sync(0xffffffffu, L.nl > C - 4)) compact<K, LB>(B, L);
-      else if (JZ_MERGE_EACH) merge<K, LB>(B, L);
+      append<K, LB>(B, L, b0, H.x);
+      append<K, LB>(B, L, b1, H.y);
+      append<K, LB>(B, L, b2, H.z);
+      append<K, LB>(B, L, b3, H.w);
+      if (__any_sync(0xffffffffu, L.nl > C - 8)) compact<K, LB>(B, L);
     }
   }
   merge<K, LB>(B, L);
 }
 
-template <int K, bool LB, bool MASK = false>
+// pad a staged batch [0, n) (n multiple of 4) with NaN sources to a multiple of 8
+template <int K>
+__device__ __forceinline__ int pad8(WarpBuf<K> &B, int n) {
+  const int lane = threadIdx.x & 31;
+  if (n & 4) {
+    if (lane < 4) {
+      const float nan = __int_as_float(0x7fc00000);
+      B.x[n + lane] = nan;
+      B.y[n + lane] = nan;
+      B.z[n + lane] = nan;
+      B.g[n + lane] = 0;
+    }
+    n += 4;
+  }
+  return n;
+}
+
+template <int K, bool LB, int MW = 0>
 __device__ __forceinline__ void eval_generic(WarpBuf<K> &B, int n, float qx, float qy, float qz, const Dom &D,
                                              Lane<K, LB> &L, int wl = 0) {
   for (int j = 0; j < n; ++j) {
     float d2 = canon_d2_per(qx, qy, qz, B.x[j], B.y[j], B.z[j], D);  // NaN padding -> NaN
-    if (MASK && (unsigned)(j - wl) < (unsigned)K) d2 = __int_as_float(0x7fc00000);
+    if constexpr (MW > 0) {
+      if ((unsigned)(j - wl) < (unsigned)MW) d2 = __int_as_float(0x7fc00000);
+    }
     append_chk<K, LB>(B, L, d2, B.g[j]);
   }
   merge<K, LB>(B, L);
@@ -453,13 +519,12 @@ __device__ __forceinline__ void visit_leaves(const LeafPK &a, const Dom &D, Warp
         ++L.stg;
         n += (m + 3) & ~3;
       }
-      __syncwarp();
       if (n == 0) continue;
-      if (!PER || c0 == 0) {
-        eval_block<K, LB, false>(B, n, qx, qy, qz, 0.f, 0.f, 0.f, L);
-      } else if (!any_straddle(c0)) {  // no axis straddles: uniform exact shift
-        eval_block<K, LB, true>(B, n, qx, qy, qz, class_shift(c0 & 3, D.L[0]), class_shift((c0 >> 2) & 3, D.L[1]),
-                                class_shift((c0 >> 4) & 3, D.L[2]), L);
+      n = pad8<K>(B, n);
+      __syncwarp();
+      if (!PER || !any_straddle(c0)) {  // no axis straddles: no wrap, or a uniform exact shift
+        eval_block<K, LB>(B, n, qx, qy, qz, PER && c0 != 0, class_shift(c0 & 3, D.L[0]),
+                          class_shift((c0 >> 2) & 3, D.L[1]), class_shift((c0 >> 4) & 3, D.L[2]), L, 0, 0);
       } else {
         eval_generic<K, LB>(B, n, qx, qy, qz, D, L);
       }
@@ -513,31 +578,68 @@ __device__ __forceinline__ void bitonic_sort_f(float (&T)[K]) {
   }
 }
 
-// z-window initialisation (self-query): the K sources at sorted positions [wpos, wpos + K)
-// around the lane's own query are evaluated first; their keys start the log and their sorted
-// values the list, so the k-th value is already close before the own leaves are scanned
-// (z-order neighbours are mostly spatial neighbours, P:L69 / Fig. 2).
+#ifndef JZ_WIN2
+#define JZ_WIN2 0
+#endif
+// window width: 2K sources for K <= 16 (the K smallest of them start the list), K for K = 32
+template <int K>
+struct WinN {
+  static constexpr int N = (JZ_WIN2 && K <= 16) ? 2 * K : K;
+};
+
+// sort a bitonic sequence ascending (half-cleaner stages)
+template <int K>
+__device__ __forceinline__ void bitonic_merge_f(float (&T)[K]) {
+#pragma unroll
+  for (int stride = K >> 1; stride > 0; stride >>= 1) {
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      const int j = i ^ stride;
+      if (j > i) {
+        const float lo = fminf(T[i], T[j]), hi = fmaxf(T[i], T[j]);
+        T[i] = lo;
+        T[j] = hi;
+      }
+    }
+  }
+}
+
+// z-window initialisation (self-query): the N = WinN<K>::N sources at sorted positions
+// [wpos, wpos + N) around the lane's own query are evaluated first; their keys start the log
+// and the K smallest values the list, so the k-th value is already close before the own
+// leaves are scanned (z-order neighbours are mostly spatial neighbours, P:L69 / Fig. 2).
 template <int K, bool LB, bool PER>
 __device__ __forceinline__ void window_init(const LeafPK &a, const Dom &D, WarpBuf<K> &B, int wpos, float qx,
                                             float qy, float qz, bool act, Lane<K, LB> &L) {
+  constexpr int N = WinN<K>::N;
+  static_assert(N <= LogCap<K>::C, "the window must fit the log");
   const int lane = threadIdx.x & 31;
-  float W[K];
+  float W0[K], W1[K];
 #pragma unroll
-  for (int o = 0; o < K; ++o) {
-    W[o] = INFINITY;
+  for (int o = 0; o < N; ++o) {
+    float d = INFINITY;
     if (act) {
       const float4 p = a.spts[wpos + o];
-      const float d = PER ? canon_d2_per(qx, qy, qz, p.x, p.y, p.z, D) : canon_d2_open(qx, qy, qz, p.x, p.y, p.z);
-      W[o] = d;
-      B.log[o][lane] = ((u64)__float_as_uint(d) << 32) | (unsigned)(__float_as_int(p.w) + 1);
+      d = PER ? canon_d2_per(qx, qy, qz, p.x, p.y, p.z, D) : canon_d2_open(qx, qy, qz, p.x, p.y, p.z);
+      B.ld[o][lane] = __float_as_uint(d);
+      B.lg[o][lane] = (unsigned)(__float_as_int(p.w) + 1);
     }
+    if (o < K) W0[o] = d;
+    else W1[o - K < K ? o - K : 0] = d;
   }
-  bitonic_sort_f<K>(W);
+  bitonic_sort_f<K>(W0);
+  if (N > K) {
+    bitonic_sort_f<K>(W1);
 #pragma unroll
-  for (int j = 0; j < K; ++j) L.F[j] = W[j];
-  L.nl = L.nf = act ? K : 0;
-  L.app += act ? K : 0;
+    for (int i = 0; i < K; ++i) W0[i] = fminf(W0[i], W1[K - 1 - i]);  // K smallest of the 2K, bitonic
+    bitonic_merge_f<K>(W0);
+  }
+#pragma unroll
+  for (int j = 0; j < K; ++j) L.F[j] = W0[j];
+  L.nl = L.nf = act ? N : 0;
+  L.app += act ? N : 0;
   L.kth = act ? L.F[K - 1] : -1.f;
+  if (N > K) compact<K, LB>(B, L);  // keep the entries <= the k-th value
 }
 
 // pre-pass over the warp's own sources [s0, s1) (the sources of the leaves holding its
@@ -559,12 +661,13 @@ __device__ __forceinline__ void own_pass(const LeafPK &a, const Dom &D, WarpBuf<
       B.g[t] = __float_as_int(p.w);
     }
     nev += act ? (unsigned)m : 0u;
+    const int np = pad8<K>(B, mp);
     __syncwarp();
     const int wl = wpos - b0;
     if (!PER || cls_all == 0) {
-      eval_block<K, LB, false, true>(B, mp, qx, qy, qz, 0.f, 0.f, 0.f, L, wl);
+      eval_block<K, LB>(B, np, qx, qy, qz, false, 0.f, 0.f, 0.f, L, WinN<K>::N, wl);
     } else {
-      eval_generic<K, LB, true>(B, mp, qx, qy, qz, D, L, wl);
+      eval_generic<K, LB, WinN<K>::N>(B, mp, qx, qy, qz, D, L, wl);
     }
     __syncwarp();
   }
@@ -638,8 +741,9 @@ __global__ void __launch_bounds__(kLThreads, JZ_MINB) k_leaf(LeafPK a, Dom D) {
     }
     const int s0o = a.sbeg[xa], s1o = a.sbeg[xb];
     int wpos = -0x40000000;  // far from every staged index: no window
-    if (!LB && a.self && a.k == K && s1o - s0o >= K) {
-      if (act) wpos = min(max(qi - K / 2, s0o), s1o - K);
+    constexpr int NW = WinN<K>::N;
+    if (!LB && a.self && a.k == K && s1o - s0o >= NW) {
+      if (act) wpos = min(max(qi - NW / 2, s0o), s1o - NW);
       window_init<K, LB, PER>(a, D, B, wpos, qx, qy, qz, act, L);
     }
     int cls_all = 0;
@@ -696,7 +800,7 @@ __global__ void __launch_bounds__(kLThreads, JZ_MINB) k_leaf(LeafPK a, Dom D) {
   if (act) {
     u64 T[K];
 #pragma unroll
-    for (int j = 0; j < K; ++j) T[j] = j < L.nl ? B.log[j][lane] : ~0ull;
+    for (int j = 0; j < K; ++j) T[j] = j < L.nl ? (((u64)B.ld[j][lane] << 32) | B.lg[j][lane]) : ~0ull;
     bitonic_sort<K>(T);
     int32_t *oi = a.out_idx + row * a.ldo + a.col0;
     float *od = a.out_d2 + row * a.ldo + a.col0;
