@@ -34,18 +34,22 @@ namespace jz {
 constexpr int kLWarps = 2;
 constexpr int kLThreads = kLWarps * 32;
 #ifndef JZ_LCAP
-#define JZ_LCAP 256
+#define JZ_LCAP 128
 #endif
 #ifndef JZ_MINB
 #define JZ_MINB 9  // 9 CTAs x 2 warps per SM: 112 registers (smem allows 9 CTAs at K = 16)
 #endif
-constexpr int kLCap = JZ_LCAP;  // staged source points per warp (4 KB SoA)
+constexpr int kLCap = JZ_LCAP;  // staged source points per warp (2 KB SoA); >= the largest leaf (kMaxLeaf)
+static_assert(JZ_LCAP >= kMaxLeaf, "a leaf must fit the staging buffer");
 
 #ifndef JZ_LOGX
-#define JZ_LOGX 16
+#define JZ_LOGX 24
 #endif
 #ifndef JZ_HALFGATE
 #define JZ_HALFGATE 1
+#endif
+#ifndef JZ_MERGE_MIN
+#define JZ_MERGE_MIN 1
 #endif
 #ifndef JZ_MERGE_EACH
 #define JZ_MERGE_EACH 0
@@ -388,7 +392,9 @@ __device__ __forceinline__ void eval_block(WarpBuf<K> &B, int n, float qx, float
       if (__any_sync(0xffffffffu, L.nl > C - 8)) compact<K, LB>(B, L);
     }
   }
-  merge<K, LB>(B, L);
+  // refresh the k-th value for the next pruning decisions once some lane has enough new
+  // entries (merge rounds = max new entries over the lanes)
+  if (__any_sync(0xffffffffu, L.nl - L.nf >= JZ_MERGE_MIN)) merge<K, LB>(B, L);
 }
 
 // pad a staged batch [0, n) (n multiple of 4) with NaN sources to a multiple of 8
@@ -516,7 +522,9 @@ __device__ __forceinline__ void visit_leaves(const LeafPK &a, const Dom &D, Warp
           B.g[n + t] = __float_as_int(p.w);
         }
         nev += act ? (unsigned)m : 0u;
+#ifndef JZ_DIAG_OWN
         ++L.stg;
+#endif
         n += (m + 3) & ~3;
       }
       if (n == 0) continue;
@@ -758,6 +766,10 @@ __global__ void __launch_bounds__(kLThreads, JZ_MINB) k_leaf(LeafPK a, Dom D) {
     }
     L.stg += xb - xa;
     own_pass<K, LB, PER>(a, D, B, s0o, s1o, cls_all, wpos, qx, qy, qz, act, L, nev);
+    if (JZ_MERGE_MIN > 1) merge<K, LB>(B, L);
+#ifdef JZ_DIAG_OWN
+    L.stg = L.rnd * 1000u + __reduce_add_sync(0xffffffffu, L.app);  // diagnostics: rounds, appends after the own pass
+#endif
   }
   const int64_t eb = a.ispl[J], ee = a.ispl[J + 1];
   for (int64_t e = eb; e < ee; ++e) {
