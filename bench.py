@@ -258,6 +258,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true", help="kernel-only run for ncu (no e2e / baseline / clocks)")
+    ap.add_argument("--order", default=None, choices=["z", "input"],
+                    help="row order under torchrun (default z: rows + global ids, P:L458; input: F2 reverse exchange)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

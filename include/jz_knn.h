@@ -212,6 +212,21 @@ JZ_API int jz_knn_select_ghosts(jz_knn_index *ix, const float *boxes, int64_t nb
 JZ_API int jz_knn_pack_ghosts(jz_knn_index *ix, const int32_t *mask, int32_t nranks, const int64_t *offsets, float *out4,
                        jz_stream_t s);
 
+/* F2 -- multi-GPU rows in input order ("final reordering step": the
+ * reverse all-to-all of the result). Step 1 (sender): the z-ordered rows of this rank
+ * (idx [m][k] int32, d2 [m][k] float32, row_gidx [m] int32, from jz_knn_query with
+ * JZ_ORDER_Z) are grouped by dest [m] int32 (the rank owning row_gidx: jz_bucket_by_splitters
+ * with the input-slice bounds as splitters) at offsets [nranks] int64 (exclusive prefix of
+ * the per-rank counts) into out [m][2k+1] int32 words: k indices, k d2 bit patterns, gidx.
+ * All pointers device; the order inside a destination group is unspecified.
+ * Step 2 (receiver, after the all-to-all-v): rows [m][2k+1] are written to out_idx /
+ * out_d2 [n][k] at row gidx - gidx_base. JZ_EDATA if a gidx lies outside
+ * [gidx_base, gidx_base + n) (nothing is guaranteed about the outputs then). Synchronises s. */
+JZ_API int jz_pack_rows(const int32_t *idx, const float *d2, const int32_t *row_gidx, int64_t m, int32_t k,
+                        const int32_t *dest, const int64_t *offsets, int32_t nranks, int32_t *out, jz_stream_t s);
+JZ_API int jz_scatter_rows(const int32_t *rows, int64_t m, int32_t k, int64_t gidx_base, int64_t n, int32_t *out_idx,
+                           float *out_d2, jz_stream_t s);
+
 /* Introspection for stage tests (copies to HOST memory dst, returns bytes needed or -1):
  * what 0 sorted keys u64[n], 1 sorted float4 points [n], 2 perm i32[n] (sorted -> input),
  * 3 plane `plane` beg i32[nnodes+1], 4 plane boxes (32 B per node), 5 plane count (int64). */

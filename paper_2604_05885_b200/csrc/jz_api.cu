@@ -246,6 +246,10 @@ jz_knn_index *build_impl(const float *pos, int64_t n, int stride, int gidx_mode,
 
 }  // namespace
 
+namespace jz {
+void set_last_error(const std::string &m) { g_err = m; }
+}  // namespace jz
+
 extern "C" {
 
 const char *jz_last_error(void) { return g_err.c_str(); }

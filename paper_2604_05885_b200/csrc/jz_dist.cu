@@ -11,6 +11,9 @@
 //                           (exact monotone box bound d_low^2 <= r2; leaf granularity is a
 //                           superset of the required points, so no neighbour can be missed)
 //   jz_knn_pack_ghosts      pack flagged points per destination rank
+//   jz_pack_rows            F2: result rows (idx[k], bits(d2)[k], gidx) grouped by the rank that
+//                           owns their input row (reverse all-to-all-v)
+//   jz_scatter_rows         F2: received rows written to input order (row = gidx - base)
 #include <climits>
 #include <vector>
 
@@ -48,6 +51,46 @@ __global__ void k_pack(const float *__restrict__ pos, int64_t n, int64_t gbase, 
     const int r = dest[i];
     const unsigned long long p = atomicAdd(&cursor[r], 1ull);
     out[off[r] + (int64_t)p] = make_float4(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2], __int_as_float((int)(gbase + i)));
+  }
+}
+
+// F2: slot of each result row in the send buffer (grouped by destination rank)
+__global__ void k_row_slots(const int32_t *__restrict__ dest, int64_t m, const int64_t *__restrict__ off,
+                            unsigned long long *__restrict__ cursor, int64_t *__restrict__ slot) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = dest[i];
+    slot[i] = off[r] + (int64_t)atomicAdd(&cursor[r], 1ull);
+  }
+}
+
+// one thread per output word: row i -> words [idx[k], bits(d2)[k], gidx] at slot[i]
+__global__ void k_pack_rows(const int32_t *__restrict__ idx, const float *__restrict__ d2,
+                            const int32_t *__restrict__ rowg, int64_t m, int k, const int64_t *__restrict__ slot,
+                            int32_t *__restrict__ out) {
+  const int W = 2 * k + 1;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < m * W; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / W;
+    const int w = (int)(t - i * W);
+    const int32_t v = w < k ? idx[i * k + w] : (w < 2 * k ? __float_as_int(d2[i * k + (w - k)]) : rowg[i]);
+    out[slot[i] * W + w] = v;
+  }
+}
+
+// one thread per received word: row j goes to input row gidx - base (flag on a bad gidx)
+__global__ void k_scatter_rows(const int32_t *__restrict__ rows, int64_t m, int k, int64_t base, int64_t n,
+                               int32_t *__restrict__ out_idx, float *__restrict__ out_d2, int *__restrict__ bad) {
+  const int W = 2 * k + 1;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < m * 2 * k; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = t / (2 * k);
+    const int w = (int)(t - j * 2 * k);
+    const int64_t row = (int64_t)rows[j * W + 2 * k] - base;
+    if (row < 0 || row >= n) {
+      *bad = 1;
+      continue;
+    }
+    const int32_t v = rows[j * W + w];
+    if (w < k) out_idx[row * k + w] = v;
+    else out_d2[row * k + (w - k)] = __int_as_float(v);
   }
 }
 
@@ -170,7 +213,7 @@ __global__ void k_ghost_pack(const float4 *__restrict__ pts, const int32_t *__re
 }  // namespace jz
 
 namespace {
-thread_local std::string g_derr;
+
 }
 
 extern "C" {
@@ -230,6 +273,57 @@ int jz_pack_by_rank(const float *pos, int64_t n, int64_t gidx_base, const int32_
   }
 }
 
+int jz_pack_rows(const int32_t *idx, const float *d2, const int32_t *row_gidx, int64_t m, int32_t k,
+                 const int32_t *dest, const int64_t *offsets, int32_t nranks, int32_t *out, jz_stream_t s) {
+  if (m < 0 || k < 1 || nranks < 1 || (m > 0 && (!idx || !d2 || !row_gidx || !dest || !offsets || !out)))
+    return JZ_EINVAL;
+  try {
+    cudaStream_t st = (cudaStream_t)s;
+    if (m == 0) return JZ_OK;
+    unsigned long long *cur = nullptr;
+    int64_t *slot = nullptr;
+    JZ_CUDA(cudaMallocAsync(&cur, nranks * sizeof(unsigned long long), st));
+    JZ_CUDA(cudaMallocAsync(&slot, m * sizeof(int64_t), st));
+    JZ_CUDA(cudaMemsetAsync(cur, 0, nranks * sizeof(unsigned long long), st));
+    jz::k_row_slots<<<jz::grid_for(m, 256), 256, 0, st>>>(dest, m, offsets, cur, slot);
+    JZ_LAUNCH_CHECK();
+    jz::k_pack_rows<<<jz::grid_for(m * (2 * k + 1), 256), 256, 0, st>>>(idx, d2, row_gidx, m, k, slot, out);
+    JZ_LAUNCH_CHECK();
+    JZ_CUDA(cudaFreeAsync(cur, st));
+    JZ_CUDA(cudaFreeAsync(slot, st));
+    return JZ_OK;
+  } catch (const jz::Error &e) {
+    jz::set_last_error(e.what());
+    return e.code;
+  }
+}
+
+int jz_scatter_rows(const int32_t *rows, int64_t m, int32_t k, int64_t gidx_base, int64_t n, int32_t *out_idx,
+                    float *out_d2, jz_stream_t s) {
+  if (m < 0 || k < 1 || n < 0 || (m > 0 && (!rows || !out_idx || !out_d2))) return JZ_EINVAL;
+  try {
+    cudaStream_t st = (cudaStream_t)s;
+    if (m == 0) return JZ_OK;
+    int *bad = nullptr;
+    JZ_CUDA(cudaMallocAsync(&bad, sizeof(int), st));
+    JZ_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), st));
+    jz::k_scatter_rows<<<jz::grid_for(m * 2 * k, 256), 256, 0, st>>>(rows, m, k, gidx_base, n, out_idx, out_d2, bad);
+    JZ_LAUNCH_CHECK();
+    int h = 0;
+    JZ_CUDA(cudaMemcpyAsync(&h, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+    JZ_CUDA(cudaFreeAsync(bad, st));
+    JZ_CUDA(cudaStreamSynchronize(st));
+    if (h) {
+      jz::set_last_error("jz_scatter_rows: a row's global index is outside [gidx_base, gidx_base + n)");
+      return JZ_EDATA;
+    }
+    return JZ_OK;
+  } catch (const jz::Error &e) {
+    jz::set_last_error(e.what());
+    return e.code;
+  }
+}
+
 int jz_knn_plane_nodes(const jz_knn_index *ix, int plane, int64_t *nnodes) {
   if (!ix || !nnodes) return JZ_EINVAL;
   jz::IndexView v = jz::view_of(ix);
@@ -267,7 +361,7 @@ int jz_knn_query_boxes(jz_knn_index *ix, int k, int plane, int rank, float *boxe
     JZ_CUDA(cudaStreamSynchronize(st));
     return JZ_OK;
   } catch (const jz::Error &e) {
-    g_derr = e.what();
+    jz::set_last_error(e.what());
     return e.code;
   }
 }
@@ -293,7 +387,7 @@ int jz_knn_select_ghosts(jz_knn_index *ix, const float *boxes, int64_t nbox, int
     }
     return JZ_OK;
   } catch (const jz::Error &e) {
-    g_derr = e.what();
+    jz::set_last_error(e.what());
     return e.code;
   }
 }
@@ -312,7 +406,7 @@ int jz_knn_pack_ghosts(jz_knn_index *ix, const int32_t *mask, int32_t nranks, co
     JZ_CUDA(cudaFreeAsync(cur, st));
     return JZ_OK;
   } catch (const jz::Error &e) {
-    g_derr = e.what();
+    jz::set_last_error(e.what());
     return e.code;
   }
 }

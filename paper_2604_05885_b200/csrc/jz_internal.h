@@ -1,6 +1,7 @@
 // jz_internal.h -- host-side structures of the CUDA path (index, planes, interaction lists).
 #pragma once
 #include <cstdint>
+#include <string>
 #include <vector>
 
 #include "../../include/jz_knn.h"
@@ -90,5 +91,8 @@ struct IndexView {
   unsigned flags;
 };
 IndexView view_of(const jz_knn_index *ix);
+
+// text returned by jz_last_error() (thread-local)
+void set_last_error(const std::string &m);
 
 }  // namespace jz

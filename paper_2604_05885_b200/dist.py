@@ -17,7 +17,10 @@ tests, or an in-process simulation that runs R logical ranks on one device). Ste
      points reachable from a peer's box (exact box bound), exchanges counts, all-to-all-v
      of ghost rows
   6. final tree over local + ghost points, queries = local points only; rows in z-order
-     with their global indices (input order is a later step, F2).
+     with their global indices (P:L458, DESIGN.md "Multi-GPU")
+  7. (order="input") reverse all-to-all-v: every row goes to the rank owning its
+     input row (splitters = the input-slice bounds), which writes it at gidx - base
+     (the paper's "final reordering step")
 
 Correctness does not depend on the partition: any point within a query's true k-th radius
 is either local or flagged as a ghost for that query's rank.
@@ -264,6 +267,23 @@ class GpuBackend:
     def query_z(self, ix, k):
         return ix.query(k, order="z")
 
+    def pack_rows(self, idx, d2, rowg, dest, counts):
+        k = idx.shape[1]
+        m = idx.shape[0]
+        off = torch.tensor(np.concatenate([[0], np.cumsum(counts)[:-1]]), dtype=torch.int64, device=idx.device)
+        out = torch.empty((max(1, m), 2 * k + 1), dtype=torch.int32, device=idx.device)
+        self.B.check(self.lib.jz_pack_rows(self.B.dptr(idx), self.B.dptr(d2), self.B.dptr(rowg), m, k,
+                                           self.B.dptr(dest), self.B.dptr(off), len(counts), self.B.dptr(out),
+                                           self._st()))
+        return out[:m]
+
+    def scatter_rows(self, rows, k, base, n, device):
+        idx = torch.empty((n, k), dtype=torch.int32, device=device)
+        d2 = torch.empty((n, k), dtype=torch.float32, device=device)
+        self.B.check(self.lib.jz_scatter_rows(self.B.dptr(rows), rows.shape[0], k, int(base), n, self.B.dptr(idx),
+                                              self.B.dptr(d2), self._st()))
+        return idx, d2
+
     def free(self, ix):
         ix.free()
 
@@ -281,12 +301,17 @@ def splitters_from_samples(all_samples: torch.Tensor, R: int, sort_fn) -> torch.
 
 
 def dist_knn(pos: torch.Tensor, gidx_base: int, k: int, box, comm: Comm, backend, n_samp: int = N_SAMP,
-             seed: int = 0, timings: dict | None = None):
+             seed: int = 0, timings: dict | None = None, order: str = "z"):
     """Exact kNN of this rank's slice against the union over ranks.
 
-    pos: this rank's [n_r, 3] float32 points (global ids gidx_base + i).
-    Returns (idx [m, k] int32 global ids, d2 [m, k] float32, row_gidx [m] int32): the rows
-    of the points this rank owns after the Morton-range partition, in z-order."""
+    pos: this rank's [n_r, 3] float32 points (global ids gidx_base + i; the slices of the
+    ranks are contiguous and in rank order).
+    order="z": returns (idx [m, k] int32 global ids, d2 [m, k] float32, row_gidx [m] int32),
+    the rows of the points this rank owns after the Morton-range partition, in z-order.
+    order="input" (F2): returns the rows of this rank's own input slice, row i = input point
+    gidx_base + i (row_gidx = gidx_base + arange(n_r))."""
+    if order not in ("z", "input"):
+        raise ValueError("order must be 'z' or 'input'")
     R, r = comm.size, comm.rank
     t = timings if timings is not None else {}
     t0 = time.perf_counter()
@@ -337,7 +362,10 @@ def dist_knn(pos: torch.Tensor, gidx_base: int, k: int, box, comm: Comm, backend
     t2 = time.perf_counter()
     if m == 0:
         z = local.new_zeros((0, k))
-        return z.to(torch.int32), z, local.new_zeros((0,), dtype=torch.int32)
+        idx, d2, rowg = z.to(torch.int32), z, local.new_zeros((0,), dtype=torch.int32)
+        if order == "input":
+            return _to_input_order(idx, d2, rowg, pos.shape[0], gidx_base, k, comm, backend)
+        return idx, d2, rowg
     allpts = torch.cat([local, ghosts]) if ghosts.shape[0] else local
     if allpts.shape[0] < k:
         raise ValueError("fewer than k points reachable on a rank (k > global n?)")
@@ -345,12 +373,38 @@ def dist_knn(pos: torch.Tensor, gidx_base: int, k: int, box, comm: Comm, backend
     idx, d2, rowg = backend.query_z(ix2, k)
     backend.free(ix2)
     t["walk"] = time.perf_counter() - t2
+    if order == "input":
+        t3 = time.perf_counter()
+        idx, d2, rowg = _to_input_order(idx, d2, rowg, pos.shape[0], gidx_base, k, comm, backend)
+        t["reorder"] = time.perf_counter() - t3
     return idx, d2, rowg
 
 
-def run_ranks_simulated(pos_np: np.ndarray, k: int, box, R: int, params=None, n_samp: int = N_SAMP):
+def _to_input_order(idx, d2, rowg, n_own, gidx_base, k, comm, backend):
+    """F2: route every z-ordered row to the rank owning its input row and write it there."""
+    R = comm.size
+    dev = idx.device
+    sizes = comm.all_gather_v(torch.tensor([n_own, gidx_base], dtype=torch.int64, device=dev))
+    sizes = [(int(x[0]), int(x[1])) for x in sizes]
+    bounds = np.concatenate([[0], np.cumsum([c for c, _ in sizes])])
+    if any(b != int(bounds[r]) for r, (_, b) in enumerate(sizes)):
+        raise ValueError("order='input' needs contiguous input slices in rank order")
+    spl = torch.tensor(bounds[1:R], dtype=torch.int64, device=dev)
+    dest, counts = backend.bucket(rowg.to(torch.int64), spl)
+    rcounts = comm.all_to_all_counts(counts)
+    send = backend.pack_rows(idx, d2, rowg, dest, counts)
+    recv = comm.all_to_all_v(send, counts, rcounts)
+    if recv.shape[0] != n_own:
+        raise RuntimeError(f"rank received {recv.shape[0]} rows for {n_own} owned input points")
+    oi, od = backend.scatter_rows(recv, k, gidx_base, n_own, dev)
+    return oi, od, torch.arange(gidx_base, gidx_base + n_own, dtype=torch.int32, device=dev)
+
+
+def run_ranks_simulated(pos_np: np.ndarray, k: int, box, R: int, params=None, n_samp: int = N_SAMP,
+                        order: str = "z"):
     """Run R logical ranks on the current CUDA device (threads + SimComm), each owning a
-    contiguous input slice. Returns the gathered rows as full arrays in input order."""
+    contiguous input slice. Returns the gathered rows as full arrays in input order (with
+    order="input" every rank already returns its own slice's rows, F2)."""
     n = pos_np.shape[0]
     bounds = [(n * i) // R for i in range(R + 1)]
     world = SimWorld(R)
@@ -364,7 +418,7 @@ def run_ranks_simulated(pos_np: np.ndarray, k: int, box, R: int, params=None, n_
             with torch.cuda.stream(st):
                 be = GpuBackend(params=params, stream=st)
                 p = torch.from_numpy(np.ascontiguousarray(pos_np[bounds[r]:bounds[r + 1]])).cuda()
-                out = dist_knn(p, bounds[r], k, box, SimComm(world, r), be, n_samp=n_samp)
+                out = dist_knn(p, bounds[r], k, box, SimComm(world, r), be, n_samp=n_samp, order=order)
                 st.synchronize()
                 res[r] = tuple(x.cpu().numpy() for x in out)
         except Exception as e:  # pragma: no cover - surfaced below
@@ -413,8 +467,10 @@ def run_bench_distributed(args, metric, unit):
     be = GpuBackend()
     from . import _binding as B
 
+    order = getattr(args, "order", None) or "z"
+
     def step():
-        return dist_knn(d_pos, lo, k, box, comm, be)
+        return dist_knn(d_pos, lo, k, box, comm, be, order=order)
 
     for _ in range(args.warmup):
         step()
@@ -435,7 +491,8 @@ def run_bench_distributed(args, metric, unit):
                 "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                 "config": {"workload": args.config, "n_points": n, "k": k, "box": "periodic L=1" if box else "open",
-                           "distribution": c["kind"], "order": "z (rows + global ids)",
+                           "distribution": c["kind"],
+                           "order": "z (rows + global ids)" if order == "z" else "input (F2 reverse all-to-all-v)",
                            "parallelism": f"Morton-range partition x{world} + ghost exchange (NCCL)"},
                 "gpu_launches": int(launches)}
         print(json.dumps(line), flush=True)

@@ -116,5 +116,20 @@ class CpuBackend:
         idx, d2 = knn_brute(p, k, ix.box, rows=rows)
         return torch.from_numpy(g[idx]), torch.from_numpy(d2), torch.from_numpy(g[:ix.n_query].copy())
 
+    def pack_rows(self, idx, d2, rowg, dest, counts):
+        order = np.argsort(dest.numpy(), kind="stable")
+        words = np.concatenate([idx.numpy(), d2.numpy().view(np.int32), rowg.numpy()[:, None]], axis=1)
+        return torch.from_numpy(np.ascontiguousarray(words[order]).astype(np.int32))
+
+    def scatter_rows(self, rows, k, base, n, device):
+        r = rows.numpy()
+        at = r[:, 2 * k].astype(np.int64) - base
+        assert ((at >= 0) & (at < n)).all()
+        idx = np.empty((n, k), np.int32)
+        d2 = np.empty((n, k), np.float32)
+        idx[at] = r[:, :k]
+        d2[at] = r[:, k:2 * k].view(np.float32)
+        return torch.from_numpy(idx), torch.from_numpy(d2)
+
     def free(self, ix):
         pass

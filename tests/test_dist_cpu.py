@@ -24,7 +24,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, n, kind, box, k, out_dir):
+def _worker(rank, world, port, n, kind, box, k, out_dir, order="z"):
     import torch.distributed as dist
 
     from paper_2604_05885_b200.dist import TorchComm, dist_knn
@@ -38,7 +38,9 @@ def _worker(rank, world, port, n, kind, box, k, out_dir):
     pos = torch.from_numpy(gen(n, 7, 1.0, start=lo, stop=hi))
     if kind == "octant":  # adversarial: everything in one corner, ranks hold each other's neighbours
         pos = pos * 0.125
-    idx, d2, rowg = dist_knn(pos, lo, k, box, TorchComm(), CpuBackend(), n_samp=64, seed=3)
+    idx, d2, rowg = dist_knn(pos, lo, k, box, TorchComm(), CpuBackend(), n_samp=64, seed=3, order=order)
+    if order == "input":  # F2: this rank's own input slice, in input order
+        assert rowg.tolist() == list(range(lo, hi))
     np.savez(os.path.join(out_dir, f"r{rank}.npz"), idx=idx.numpy(), d2=d2.numpy(), rowg=rowg.numpy())
     dist.destroy_process_group()
 
@@ -63,6 +65,20 @@ def test_gloo_dist_knn_equals_oracle(world, kind, box):
     if kind == "octant":
         pos = (pos * 0.125).astype(np.float32)
     io, do = knn_brute(pos, k, box)
+    assert np.array_equal(idx, io)
+    assert np.array_equal(d2.view(np.int32), do.view(np.int32))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_dist_knn_input_order(world):
+    """F2: rows routed back to the rank owning their input row (reverse all-to-all-v)."""
+    n, k = 1200, 8
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_worker, args=(world, _free_port(), n, "clustered", 1.0, k, d, "input"), nprocs=world, join=True)
+        parts = [np.load(os.path.join(d, f"r{r}.npz")) for r in range(world)]
+    idx = np.concatenate([z["idx"] for z in parts])
+    d2 = np.concatenate([z["d2"] for z in parts])
+    io, do = knn_brute(clustered_points(n, 7, 1.0), k, 1.0)
     assert np.array_equal(idx, io)
     assert np.array_equal(d2.view(np.int32), do.view(np.int32))
 

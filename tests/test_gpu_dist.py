@@ -41,3 +41,30 @@ def test_simulated_octant_and_wrap():
     idx, d2, _ = run_ranks_simulated(q, 16, 1.0, 8)
     io, do = knn_grid(q, 16, 1.0)
     assert np.array_equal(idx, io) and np.array_equal(d2, do)
+
+
+@pytest.mark.parametrize("R", [1, 2, 4, 8])
+def test_simulated_ranks_input_order(R):
+    """F2: every logical rank returns its own input slice's rows (reverse all-to-all-v through
+    jz_bucket_by_splitters / jz_pack_rows / jz_scatter_rows), concatenated = the oracle."""
+    from paper_2604_05885_b200.dist import run_ranks_simulated
+
+    pos = clustered_points(120_000, 23, 1.0)
+    idx, d2, owned = run_ranks_simulated(pos, 16, 1.0, R, order="input")
+    assert owned == [(len(pos) * (r + 1)) // R - (len(pos) * r) // R for r in range(R)]
+    io, do = knn_grid(pos, 16, 1.0)
+    assert np.array_equal(idx, io)
+    assert np.array_equal(d2.view(np.int32), do.view(np.int32))
+
+
+def test_scatter_rows_rejects_foreign_rows():
+    import torch
+
+    from paper_2604_05885_b200 import _binding as B
+
+    rows = torch.zeros((2, 5), dtype=torch.int32, device="cuda")
+    rows[:, 4] = torch.tensor([10, 99], dtype=torch.int32)
+    oi = torch.empty((5, 2), dtype=torch.int32, device="cuda")
+    od = torch.empty((5, 2), dtype=torch.float32, device="cuda")
+    rc = B.lib().jz_scatter_rows(B.dptr(rows), 2, 2, 10, 5, B.dptr(oi), B.dptr(od), None)
+    assert rc == B.JZ_EDATA and b"outside" in B.lib().jz_last_error()
