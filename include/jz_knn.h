@@ -71,7 +71,10 @@ typedef struct {
   uint32_t flags;  /* JZ_FLAG_* */
   float frame_origin[3]; /* with JZ_FLAG_FRAME: key frame origin (open boundary) */
   float frame_extent;    /* with JZ_FLAG_FRAME: key frame edge length (> 0) */
-  int32_t reserved[4];
+  int32_t reg_fmax;      /* regularisation f_max: 0 => off; > 0 => every plane also splits
+                            the gaps whose Morton level exceeds lvl_max^(p), 2^lvl_max <= f_max V_90%^(p)
+                            (paper: f_max ~ 50). Structure only: results are identical either way. */
+  int32_t reserved[3];
 } jz_knn_params;
 
 /*

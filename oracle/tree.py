@@ -15,6 +15,10 @@ asks). Slow, obviously-correct loops; no blocking or reordering.
   super_splits     P:L315      Range(0, N_top, NGR)
   radius_of_count  P:L380      smallest radius with cumulative count >= k, else inf
   countheap_insert P:L380      ordered insert, drop last, or merge count (see below)
+  node_level       P:L120-124  Morton level of a node: bitlen(first key xor last key); volume 2^lvl
+  v90              P:L264-266  point-weighted mean volume of the smallest nodes holding 90% of points
+  level_max        P:L260-263  V_max = 2^lvl_max = f_max V_90%: the largest lvl with 2^lvl <= f_max V_90%
+  build_hierarchy_reg P:L257-263 regularisation: also split every gap whose level exceeds lvl_max^(p)
 """
 from __future__ import annotations
 
@@ -189,3 +193,68 @@ def countheap_insert(heap, r, cnt, k, cap=8):
     else:
         h[-1] = (r, h[-1][1] + cnt)
     return h
+
+
+# ----------------------------------------------------------------------------- regularisation
+# PAPER.md §2.4 "Regularization". Readings (R18-R20): the volume of a node
+# is 2^lvl with lvl its Morton level in bits (the smallest Morton cell holding its first and last
+# key; a single point has level 0); V_90%^(p) is computed over the count-based nodes
+# of plane p (before any forced split), taken in order of (volume, index) until their cumulative
+# point count reaches 90% of all points (the node that crosses 90% is included); lvl_max^(p) is
+# made non-decreasing in p so the planes stay nested; f_max is an integer (paper: ~50).
+
+
+def node_level(keys, a, b):
+    """Morton level of the node of sorted points [a, b) (b > a)."""
+    return key_level(keys[a], keys[b - 1])
+
+
+def v90(levels, counts):
+    """P:L264-266 as an exact rational (num, den): sum(n_i 2^lvl_i) / sum(n_i) over the smallest
+    nodes (by 2^lvl, ties by index) that together contain 90% of all points."""
+    total = sum(int(c) for c in counts)
+    num = den = 0
+    for i in sorted(range(len(levels)), key=lambda j: (int(levels[j]), j)):
+        num += int(counts[i]) << int(levels[i])
+        den += int(counts[i])
+        if 10 * den >= 9 * total:
+            break
+    return num, den
+
+
+def level_max(levels, counts, fmax):
+    """the largest integer lvl with 2^lvl <= f_max * V_90% (exact integer arithmetic)."""
+    num, den = v90(levels, counts)
+    lvl = 0
+    while (1 << (lvl + 1)) * den <= int(fmax) * num:
+        lvl += 1
+    return lvl
+
+
+def build_hierarchy_reg(keys, nmax0=48, c=8, ntarget=1000, fmax=50):
+    """Regularised planes: plane p keeps the gaps with n > N_max^(p) and
+    also every gap whose level exceeds lvl_max^(p). Returns (leaf split gaps, [plane p >= 1 splits
+    as indices into plane p-1's split array], n per gap, [lvl_max^(p)])."""
+    keys = [int(k) for k in keys]
+    n = len(keys)
+    n_of_gap = node_ranges(keys)
+    lvl = pair_levels(keys)
+    sched = plane_schedule(n, nmax0, c, ntarget)
+
+    def lvl_max_of(splits):
+        lv = [node_level(keys, a, b) for a, b in zip(splits[:-1], splits[1:])]
+        ct = [b - a for a, b in zip(splits[:-1], splits[1:])]
+        return level_max(lv, ct, fmax)
+
+    lm = lvl_max_of(tree_plane(n_of_gap, sched[0]))
+    spl0 = [g for g in range(n + 1) if n_of_gap[g] > sched[0] or lvl[g] > lm]
+    lms = [lm]
+    planes = []
+    gaps = spl0
+    for nm in sched[1:]:
+        lm = max(lvl_max_of([g for g in gaps if n_of_gap[g] > nm]), lm)
+        idx = [j for j, g in enumerate(gaps) if n_of_gap[g] > nm or lvl[g] > lm]
+        planes.append(idx)
+        gaps = [gaps[j] for j in idx]
+        lms.append(lm)
+    return spl0, planes, n_of_gap, lms

@@ -34,7 +34,8 @@ class Params(ctypes.Structure):
         ("flags", ctypes.c_uint32),
         ("frame_origin", ctypes.c_float * 3),
         ("frame_extent", ctypes.c_float),
-        ("reserved", ctypes.c_int32 * 4),
+        ("reg_fmax", ctypes.c_int32),
+        ("reserved", ctypes.c_int32 * 3),
     ]
 
 

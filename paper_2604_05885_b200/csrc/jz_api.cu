@@ -206,6 +206,7 @@ jz_knn_index *build_impl(const float *pos, int64_t n, int stride, int gidx_mode,
   jz_knn_params prm = normalize(p);
   if (prm.nmax0 > jz::kMaxLeaf) throw jz::Error(JZ_EINVAL, "nmax0 must be <= 128");
   if (prm.coarsen < 2) throw jz::Error(JZ_EINVAL, "coarsen must be >= 2");
+  if (prm.reg_fmax < 0) throw jz::Error(JZ_EINVAL, "reg_fmax must be >= 0");
   if ((prm.flags & JZ_FLAG_FRAME) && !(prm.frame_extent > 0.f)) throw jz::Error(JZ_EINVAL, "frame_extent must be > 0");
   init_pool();
   auto *ix = new jz_knn_index();

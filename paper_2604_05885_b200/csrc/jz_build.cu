@@ -222,6 +222,123 @@ __global__ void k_node_boxes(const NodeBox *__restrict__ child, const int32_t *_
   }
 }
 
+// ---------------------------------------------------------------- regularisation
+// PAPER.md §2.4 "Regularization", readings DESIGN.md R18-R20: node volume 2^lvl with
+// lvl = bitlen(first key ^ last key); V_90% over the count-based nodes of the plane in (volume,
+// index) order until 90% of the points are covered (the crossing node included); lvl_max = the
+// largest l with 2^l <= f_max V_90% (exact integer arithmetic); non-decreasing over planes; every
+// gap (leaf plane) or leaf split (plane p >= 1) with a level above lvl_max becomes a split.
+__device__ __forceinline__ int gap_level(const uint64_t *__restrict__ keys, int64_t n, int64_t g) {
+  return (g <= 0 || g >= n) ? kLevelSentinel : 64 - __clzll((long long)(keys[g - 1] ^ keys[g]));
+}
+
+// node i = sorted points [beg[s(i)], beg[s(i+1)]) with s = leafspl (planes >= 1) or identity
+__global__ void k_node_levels(const uint64_t *__restrict__ keys, const int32_t *__restrict__ beg,
+                              const int32_t *__restrict__ leafspl, int64_t nnodes, uint8_t *__restrict__ lvl,
+                              int32_t *__restrict__ cnt, unsigned long long *__restrict__ hist) {
+  __shared__ unsigned long long s_h[kLevelSentinel + 1];
+  for (int i = threadIdx.x; i <= kLevelSentinel; i += blockDim.x) s_h[i] = 0;
+  __syncthreads();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nnodes; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = beg[leafspl ? leafspl[i] : i], b = beg[leafspl ? leafspl[i + 1] : i + 1];
+    const int c = (int)(b - a);
+    const int l = c >= 2 ? 64 - __clzll((long long)(keys[a] ^ keys[b - 1])) : 0;
+    lvl[i] = (uint8_t)l;
+    cnt[i] = c;
+    atomicAdd(&s_h[l], (unsigned long long)c);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i <= kLevelSentinel; i += blockDim.x)
+    if (s_h[i]) atomicAdd(&hist[i], s_h[i]);
+}
+
+__global__ void k_level_select(const uint8_t *__restrict__ lvl, const int32_t *__restrict__ cnt, int64_t m, int b,
+                               int32_t *__restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = lvl[i] == b ? cnt[i] : 0;
+}
+
+// first node (index order) of level b whose inclusive prefix count reaches rem
+__global__ void k_first_reach(const uint8_t *__restrict__ lvl, const int32_t *__restrict__ cnt,
+                              const int64_t *__restrict__ pre, int64_t m, int b, int64_t rem,
+                              unsigned long long *__restrict__ best) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+    if (lvl[i] == b && pre[i] + cnt[i] >= rem) atomicMin(best, (unsigned long long)i);
+}
+
+__global__ void k_force_gaps(const uint64_t *__restrict__ keys, int64_t n, int lm, int32_t *__restrict__ flag) {
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g <= n; g += (int64_t)gridDim.x * blockDim.x)
+    if (gap_level(keys, n, g) > lm) flag[g] = 1;
+}
+
+__global__ void k_force_splits(const uint64_t *__restrict__ keys, int64_t n, const int32_t *__restrict__ leafbeg,
+                               const int32_t *__restrict__ leafspl_prev, int64_t m, int lm,
+                               int32_t *__restrict__ flag) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += (int64_t)gridDim.x * blockDim.x)
+    if (gap_level(keys, n, leafbeg[leafspl_prev[j]]) > lm) flag[j] = 1;
+}
+
+// lvl_max of the nodes [beg[s(i)], beg[s(i+1)]), host-side exact arithmetic
+static int level_max_of(const uint64_t *keys, const int32_t *beg, const int32_t *leafspl, int64_t nnodes, int fmax,
+                        cudaStream_t st) {
+  typedef unsigned __int128 u128;
+  uint8_t *lvl = nullptr;
+  int32_t *cnt = nullptr, *sel = nullptr;
+  int64_t *pre = nullptr;
+  unsigned long long *hist = nullptr;
+  JZ_CUDA(cudaMallocAsync(&lvl, nnodes, st));
+  JZ_CUDA(cudaMallocAsync(&cnt, nnodes * sizeof(int32_t), st));
+  JZ_CUDA(cudaMallocAsync(&hist, (kLevelSentinel + 2) * sizeof(unsigned long long), st));
+  JZ_CUDA(cudaMemsetAsync(hist, 0, (kLevelSentinel + 1) * sizeof(unsigned long long), st));
+  k_node_levels<<<grid_for(nnodes, 256), 256, 0, st>>>(keys, beg, leafspl, nnodes, lvl, cnt, hist);
+  JZ_LAUNCH_CHECK();
+  unsigned long long h[kLevelSentinel + 1];
+  JZ_CUDA(cudaMemcpyAsync(h, hist, sizeof(h), cudaMemcpyDeviceToHost, st));
+  JZ_CUDA(cudaStreamSynchronize(st));
+  u128 total = 0;
+  for (int l = 0; l <= kLevelSentinel; ++l) total += h[l];
+  u128 cum = 0, num = 0;
+  int b = 0;
+  for (; b <= kLevelSentinel; ++b) {
+    if (10 * (cum + h[b]) >= 9 * total) break;
+    cum += h[b];
+    num += (u128)h[b] << b;
+  }
+  // part of level b: the shortest index-order prefix of its nodes reaching the 90% mark
+  const int64_t rem = (int64_t)((9 * total - 10 * cum + 9) / 10);
+  u128 part = 0;
+  if (rem > 0) {
+    JZ_CUDA(cudaMallocAsync(&sel, nnodes * sizeof(int32_t), st));
+    JZ_CUDA(cudaMallocAsync(&pre, (nnodes + 1) * sizeof(int64_t), st));
+    k_level_select<<<grid_for(nnodes, 256), 256, 0, st>>>(lvl, cnt, nnodes, b, sel);
+    JZ_LAUNCH_CHECK();
+    exclusive_scan_i32_to_i64(sel, pre, nnodes, st);
+    unsigned long long *best = hist + kLevelSentinel + 1;
+    const unsigned long long inf = ~0ull;
+    JZ_CUDA(cudaMemcpyAsync(best, &inf, sizeof(inf), cudaMemcpyHostToDevice, st));
+    k_first_reach<<<grid_for(nnodes, 256), 256, 0, st>>>(lvl, cnt, pre, nnodes, b, rem, best);
+    JZ_LAUNCH_CHECK();
+    unsigned long long ib = 0;
+    JZ_CUDA(cudaMemcpyAsync(&ib, best, sizeof(ib), cudaMemcpyDeviceToHost, st));
+    JZ_CUDA(cudaStreamSynchronize(st));
+    int64_t pv = 0;
+    int32_t cv = 0;
+    JZ_CUDA(cudaMemcpy(&pv, pre + ib, sizeof(pv), cudaMemcpyDeviceToHost));
+    JZ_CUDA(cudaMemcpy(&cv, cnt + ib, sizeof(cv), cudaMemcpyDeviceToHost));
+    part = (u128)(pv + cv);
+    JZ_CUDA(cudaFreeAsync(sel, st));
+    JZ_CUDA(cudaFreeAsync(pre, st));
+  }
+  num += part << b;
+  const u128 den = cum + part;
+  int lm = 0;
+  while (lm < 120 && ((u128)1 << (lm + 1)) * den <= (u128)fmax * num) ++lm;
+  JZ_CUDA(cudaFreeAsync(lvl, st));
+  JZ_CUDA(cudaFreeAsync(cnt, st));
+  JZ_CUDA(cudaFreeAsync(hist, st));
+  return lm;
+}
+
 void free_planes(std::vector<Plane> &planes, cudaStream_t st) {
   for (auto &p : planes) {
     if (p.beg) cudaFreeAsync(p.beg, st);
@@ -243,15 +360,31 @@ void build_planes(const uint64_t *keys, const float4 *pts, int64_t n, const jz_k
   k_leaf_flags<<<fb, kFlagBlock, (kFlagBlock + 2 * W + 2) * sizeof(uint64_t), st>>>(keys, n, W, flag);
   JZ_LAUNCH_CHECK();
   exclusive_scan_i32_to_i64(flag, pos, n + 1, st);
-  const int64_t nspl = read_i64(pos + (n + 1), st);  // = N_leaf + 1
+  int64_t nspl = read_i64(pos + (n + 1), st);  // = N_leaf + 1
   Plane leaf;
   leaf.nnodes = nspl - 1;
   leaf.nmax = W;
   JZ_CUDA(cudaMallocAsync(&leaf.beg, nspl * sizeof(int32_t), st));
-  JZ_CUDA(cudaMallocAsync(&leaf.leafspl, nspl * sizeof(int32_t), st));
-  JZ_CUDA(cudaMallocAsync(&leaf.box, leaf.nnodes * sizeof(NodeBox), st));
   k_compact_gaps<<<grid_for(n + 1, 256), 256, 0, st>>>(flag, pos, n + 1, leaf.beg);
   JZ_LAUNCH_CHECK();
+  const int fmax = prm.reg_fmax;
+  if (fmax > 0) {  // regularisation of the leaf plane
+    leaf.lvl_max = level_max_of(keys, leaf.beg, nullptr, leaf.nnodes, fmax, st);
+    k_force_gaps<<<grid_for(n + 1, 256), 256, 0, st>>>(keys, n, leaf.lvl_max, flag);
+    JZ_LAUNCH_CHECK();
+    exclusive_scan_i32_to_i64(flag, pos, n + 1, st);
+    const int64_t nspl2 = read_i64(pos + (n + 1), st);
+    if (nspl2 != nspl) {
+      JZ_CUDA(cudaFreeAsync(leaf.beg, st));
+      nspl = nspl2;
+      leaf.nnodes = nspl - 1;
+      JZ_CUDA(cudaMallocAsync(&leaf.beg, nspl * sizeof(int32_t), st));
+      k_compact_gaps<<<grid_for(n + 1, 256), 256, 0, st>>>(flag, pos, n + 1, leaf.beg);
+      JZ_LAUNCH_CHECK();
+    }
+  }
+  JZ_CUDA(cudaMallocAsync(&leaf.leafspl, nspl * sizeof(int32_t), st));
+  JZ_CUDA(cudaMallocAsync(&leaf.box, leaf.nnodes * sizeof(NodeBox), st));
   k_iota<<<grid_for(nspl, 256), 256, 0, st>>>(leaf.leafspl, nspl);
   JZ_LAUNCH_CHECK();
   int32_t *nsplit = nullptr;
@@ -272,15 +405,33 @@ void build_planes(const uint64_t *keys, const float4 *pts, int64_t n, const jz_k
     k_plane_flags<<<grid_for(m, 256), 256, 0, st>>>(pv.leafspl, m, nsplit, nmax, flag);
     JZ_LAUNCH_CHECK();
     exclusive_scan_i32_to_i64(flag, pos, m, st);
-    const int64_t np1 = read_i64(pos + m, st);
+    int64_t np1 = read_i64(pos + m, st);
     Plane pl;
     pl.nnodes = np1 - 1;
     pl.nmax = nmax;
     JZ_CUDA(cudaMallocAsync(&pl.beg, np1 * sizeof(int32_t), st));
     JZ_CUDA(cudaMallocAsync(&pl.leafspl, np1 * sizeof(int32_t), st));
-    JZ_CUDA(cudaMallocAsync(&pl.box, pl.nnodes * sizeof(NodeBox), st));
     k_plane_compact<<<grid_for(m, 256), 256, 0, st>>>(flag, pos, pv.leafspl, m, pl.beg, pl.leafspl);
     JZ_LAUNCH_CHECK();
+    if (fmax > 0) {  // regularisation of plane p, lvl_max non-decreasing (nesting)
+      const int lm = level_max_of(keys, planes[0].beg, pl.leafspl, pl.nnodes, fmax, st);
+      pl.lvl_max = lm > pv.lvl_max ? lm : pv.lvl_max;
+      k_force_splits<<<grid_for(m, 256), 256, 0, st>>>(keys, n, planes[0].beg, pv.leafspl, m, pl.lvl_max, flag);
+      JZ_LAUNCH_CHECK();
+      exclusive_scan_i32_to_i64(flag, pos, m, st);
+      const int64_t np2 = read_i64(pos + m, st);
+      if (np2 != np1) {
+        JZ_CUDA(cudaFreeAsync(pl.beg, st));
+        JZ_CUDA(cudaFreeAsync(pl.leafspl, st));
+        np1 = np2;
+        pl.nnodes = np1 - 1;
+        JZ_CUDA(cudaMallocAsync(&pl.beg, np1 * sizeof(int32_t), st));
+        JZ_CUDA(cudaMallocAsync(&pl.leafspl, np1 * sizeof(int32_t), st));
+        k_plane_compact<<<grid_for(m, 256), 256, 0, st>>>(flag, pos, pv.leafspl, m, pl.beg, pl.leafspl);
+        JZ_LAUNCH_CHECK();
+      }
+    }
+    JZ_CUDA(cudaMallocAsync(&pl.box, pl.nnodes * sizeof(NodeBox), st));
     k_node_boxes<<<grid_for(pl.nnodes * 32, 256), 256, 0, st>>>(pv.box, pl.beg, pl.nnodes, pl.box);
     JZ_LAUNCH_CHECK();
     planes.push_back(pl);

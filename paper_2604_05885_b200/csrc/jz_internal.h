@@ -21,6 +21,7 @@ struct Plane {
   int32_t *beg = nullptr;     // [nnodes + 1] (device)
   int32_t *leafspl = nullptr; // [nnodes + 1] index into the leaf split array (device); p = 0: identity
   NodeBox *box = nullptr;     // [nnodes] (device)
+  int lvl_max = -1;           // regularisation level bound of the plane, -1 = off
 };
 
 struct Stage {

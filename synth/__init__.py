@@ -8,6 +8,7 @@ from .generators import (  # noqa: F401
     splitmix64,
     uniform_points,
     clustered_points,
+    normal_points,
     lattice_points,
     make_config,
     CONFIGS,

@@ -182,6 +182,30 @@ def _parallel_chunks(fn, start, stop, chunk=1 << 20):
         list(ex.map(lambda s: fn(*s), spans))
 
 
+# fixed lower-triangular factor of the normal workload's covariance (correlated axes)
+_NORMAL_A = np.array([[1.0, 0.0, 0.0], [0.5, 0.8, 0.0], [0.2, -0.3, 0.6]])
+
+
+def normal_points(n: int, seed: int, box=None, start: int = 0, stop: int | None = None) -> np.ndarray:
+    """Rows [start, stop) of the multivariate normal set of size n (PAPER.md L453 scenario (3),
+    the outlier-heavy case of the regularisation, L257): x = A z, z ~ N(0, I) by double-precision
+    Box-Muller, rounded to float32; open domain (`box` is ignored)."""
+    stop = n if stop is None else stop
+    out = np.empty((stop - start, 3), dtype=np.float32)
+
+    def work(c0, c1):
+        idx = np.arange(c0, c1, dtype=np.uint64)
+        z = np.empty((c1 - c0, 3))
+        for d in range(3):
+            u1 = _u53(seed, _STREAM_POINT, idx, 2 * d, 8)
+            u2 = _u53(seed, _STREAM_POINT, idx, 2 * d + 1, 8)
+            z[:, d] = np.sqrt(-2.0 * np.log(u1)) * np.cos(2.0 * math.pi * u2)
+        out[c0 - start:c1 - start] = (z @ _NORMAL_A.T).astype(np.float32)
+
+    _parallel_chunks(work, start, stop)
+    return out
+
+
 def lattice_points(n_side: int, h: float = 1.0 / 16.0, jitter_order: bool = False) -> np.ndarray:
     """n_side^3 cubic lattice with spacing h; index = (ix * n + iy) * n + iz."""
     g = np.arange(n_side, dtype=np.float64) * h
@@ -197,6 +221,8 @@ CONFIGS = {
     "C3": dict(n=10_000_000, kind="clustered", box=1.0, k=32, seed=3),
     "C4": dict(n=100_000_000, kind="clustered", box=1.0, k=16, seed=4),
     "C5": dict(n=1 << 30, kind="uniform", box=1.0, k=8, seed=5),
+    # aux (not a BASELINE config): the multivariate normal scenario of P:L453 / regularisation P:L257
+    "N1": dict(n=10_000_000, kind="normal", box=None, k=16, seed=6),
 }
 
 
@@ -208,6 +234,6 @@ def make_config(name: str, n: int | None = None, start: int = 0, stop: int | Non
     c = dict(CONFIGS[name])
     if n is not None:
         c["n"] = n
-    gen = uniform_points if c["kind"] == "uniform" else clustered_points
+    gen = {"uniform": uniform_points, "clustered": clustered_points, "normal": normal_points}[c["kind"]]
     pts = gen(c["n"], c["seed"], box=c["box"] if c["box"] is not None else 1.0, start=start, stop=stop)
     return pts, c["box"], c["k"]

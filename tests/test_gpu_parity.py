@@ -232,6 +232,39 @@ def test_stage_planes_vs_oracle_tree(kind):
     ix.free()
 
 
+@pytest.mark.parametrize("kind,fmax", [("normal", 50), ("normal", 4), ("clustered", 2), ("uniform", 50)])
+def test_stage_regularised_planes_vs_oracle(kind, fmax):
+    """F3: with reg_fmax the GPU planes equal the oracle's regularised hierarchy
+    (lvl_max^(p) from V_90%^(p), forced splits above it) on the same sorted keys; small f_max
+    forces many splits, f_max = 50 on uniform points none."""
+    from synth import normal_points
+
+    jz = _jz()
+    gen = {"normal": normal_points, "clustered": clustered_points, "uniform": uniform_points}[kind]
+    pos = gen(3000, 31, 1.0)
+    box = 1.0 if kind != "normal" else None
+    prm = dict(nmax0=16, coarsen=3, ntarget=20, reg_fmax=fmax)
+    ix = jz.KnnIndex(torch.from_numpy(pos).cuda(), box=box, params=prm)
+    keys = ix.sorted_keys()
+    spl0, planes, _, _ = T.build_hierarchy_reg(keys, nmax0=16, c=3, ntarget=20, fmax=fmax)
+    assert ix.num_planes() == 1 + len(planes)
+    assert ix.plane_beg(0).tolist() == spl0
+    for p, want in enumerate(planes, start=1):
+        assert ix.plane_beg(p).tolist() == want
+    ix.free()
+
+
+@pytest.mark.parametrize("fmax", [50, 2])
+def test_regularised_knn_bit_exact(fmax):
+    """F3: regularisation changes the tree, never the result (multivariate normal, P:L453 (3))."""
+    from synth import normal_points
+
+    pos = normal_points(30000, 32)
+    ig, dg = _gpu_knn(pos, 16, None, params=dict(reg_fmax=fmax))
+    io, do = knn_brute(pos, 16, None)
+    _assert_same(ig, dg, io, do)
+
+
 # ----------------------------------------------------------------------------------- larger configs
 
 

@@ -161,3 +161,60 @@ def test_countheap_radius_is_upper_bound():
             assert true_cnt >= k
         else:
             assert sum(c for _, c in items) < k  # every item was inserted; counts are conserved
+
+
+# ------------------------------------------------------------------ regularisation
+def test_reg_v90_hand_examples():
+    """P:L260-266 worked by hand: four level-3 nodes of 4 points and a level-20 outlier node of 1:
+    the smallest nodes reach 16/17 >= 90% without the outlier, so V_90% = 2^3 = 8 and
+    f_max = 50 gives V_max = 400 -> lvl_max = 8 (2^8 = 256 <= 400 < 512)."""
+    assert T.v90([3, 3, 3, 3, 20], [4, 4, 4, 4, 1]) == (128, 16)
+    assert T.level_max([3, 3, 3, 3, 20], [4, 4, 4, 4, 1], 50) == 8
+    assert T.level_max([3, 3, 3, 3, 20], [4, 4, 4, 4, 1], 1) == 3
+    # ties in volume are taken in index order; the node crossing 90% is included:
+    # total 21, 0.9 * 21 = 18.9 -> nodes (lvl 2, n 1), (lvl 5, n 10), (lvl 5, n 10)
+    assert T.v90([5, 2, 5], [10, 1, 10]) == (4 + 320 + 320, 21)
+    assert T.level_max([5, 2, 5], [10, 1, 10], 50) == 10  # 50 * 644 / 21 = 1533.3 -> 2^10
+
+
+def _keys_of(pos, box=None):
+    o, s = T.key_frame(pos, box)
+    return np.sort(T.morton_keys(T.quantize(pos, o, s, is_scale=True)))
+
+
+def test_reg_splits_isolate_outliers():
+    """a multivariate normal set (P:L453 (3)): count-based leaves in the sparse tails span
+    huge Morton cells; the regularised plane splits every gap above lvl_max, so every node of >= 2 points has
+    level <= lvl_max (its level is its largest interior gap), it refines the count-based plane,
+    and here it has more leaves."""
+    from synth import normal_points
+
+    keys = [int(k) for k in _keys_of(normal_points(3000, 6))]
+    n_of_gap = T.node_ranges(keys)
+    base = T.tree_plane(n_of_gap, 48)
+    spl0, planes, _, lms = T.build_hierarchy_reg(keys, nmax0=48, c=8, ntarget=1, fmax=50)
+    assert set(base) <= set(spl0) and len(spl0) > len(base)
+    for a, b in zip(spl0[:-1], spl0[1:]):
+        if b - a >= 2:
+            assert T.node_level(keys, a, b) <= lms[0]
+    big = max(T.node_level(keys, a, b) for a, b in zip(base[:-1], base[1:]))
+    assert big > lms[0]  # without the regularisation some leaf exceeds V_max
+    gaps = spl0
+    for p, idx in enumerate(planes):  # nested, and the level bound holds on every plane
+        sub = [gaps[j] for j in idx]
+        assert set(sub) <= set(gaps) and lms[p + 1] >= lms[p]
+        for a, b in zip(sub[:-1], sub[1:]):
+            if b - a >= 2:
+                assert T.node_level(keys, a, b) <= lms[p + 1]
+        gaps = sub
+
+
+def test_reg_uniform_unchanged():
+    """for uniform random points the count-based structure is already regular:
+    f_max = 50 adds no split."""
+    from synth import uniform_points
+
+    keys = [int(k) for k in _keys_of(uniform_points(4000, 9, 1.0), 1.0)]
+    spl0, planes, n_of_gap, _ = T.build_hierarchy_reg(keys, nmax0=48, c=8, ntarget=10, fmax=50)
+    s0, p0, _ = T.build_hierarchy(keys, nmax0=48, c=8, ntarget=10)
+    assert spl0 == s0 and planes == p0
