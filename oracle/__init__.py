@@ -12,5 +12,9 @@ Contents
            notation (Morton keys, pair levels, node ranges by binary search,
            tree planes, dense interaction list, count heap) -- PAPER.md §2.3-§3.2.
            Used to pin the CUDA build stages stage by stage.
+  knn.py   also friends-of-friends by definition (§5):
+           connected components of d2 <= RN32(r_link^2), labels = component minima,
+           brute force and a grid variant (C), and the group catalogue (numpy FP64).
 """
 from .knn import knn_brute, knn_grid, pair_d2, build_oracle, oracle_threads  # noqa: F401
+from .knn import fof_b2, fof_labels, fof_catalogue  # noqa: F401

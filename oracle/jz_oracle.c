@@ -356,3 +356,137 @@ void oracle_pair_d2(const float *a, const float *b, int64_t m, const float *box,
   make_domain(&dom, box);
   for (int64_t i = 0; i < m; ++i) out[i] = canon_d2(a + 3 * i, b + 3 * i, &dom);
 }
+
+/* ------------------------------------------------------------------------- */
+/* Friends-of-friends (§5)              */
+/* ------------------------------------------------------------------------- */
+/*
+ * Groups are the connected components of the graph with an edge between i != j
+ * iff the canonical FP32 d2(p_i, p_j) (above) is <= b2, b2 = RN32(r_link * r_link)
+ * (R21). label[i] = the smallest index of i's component: the union-find
+ * below always links the larger root under the smaller one ("update the
+ * higher index root to point towards the lower index root"), so every root is its
+ * component's minimum.
+ *   oracle_fof_brute : every pair i < j, O(N^2).
+ *   oracle_fof_grid  : cells of width >= 1.0001 r_link, pairs in the 27 neighbouring
+ *                      cells (a linked pair is closer than one cell width on every
+ *                      axis); same labels (pinned against brute in tests).
+ */
+static int32_t uf_find(int32_t *par, int32_t x) {
+  while (par[x] != x) {
+    par[x] = par[par[x]];
+    x = par[x];
+  }
+  return x;
+}
+
+static void uf_union(int32_t *par, int32_t a, int32_t b) {
+  a = uf_find(par, a);
+  b = uf_find(par, b);
+  if (a == b) return;
+  if (a < b)
+    par[b] = a;
+  else
+    par[a] = b;
+}
+
+static void uf_labels(int32_t *par, int64_t n) {
+  for (int64_t i = 0; i < n; ++i) par[i] = uf_find(par, (int32_t)i);
+}
+
+int oracle_fof_brute(const float *pos, int64_t n, const float *box, float b2, int32_t *label) {
+  domain_t dom;
+  make_domain(&dom, box);
+  for (int64_t i = 0; i < n; ++i) label[i] = (int32_t)i;
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = i + 1; j < n; ++j)
+      if (canon_d2(pos + 3 * i, pos + 3 * j, &dom) <= b2) uf_union(label, (int32_t)i, (int32_t)j);
+  uf_labels(label, n);
+  return 0;
+}
+
+int oracle_fof_grid(const float *pos, int64_t n, const float *box, float b2, int32_t *label) {
+  domain_t dom;
+  make_domain(&dom, box);
+  const double w = sqrt((double)b2) * 1.0001;
+  double lo[3], span[3];
+  for (int d = 0; d < 3; ++d) {
+    lo[d] = dom.periodic ? 0.0 : INFINITY;
+    span[d] = dom.periodic ? dom.L[d] : -INFINITY;
+  }
+  if (!dom.periodic) {
+    double hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int64_t i = 0; i < n; ++i)
+      for (int d = 0; d < 3; ++d) {
+        if (pos[3 * i + d] < lo[d]) lo[d] = pos[3 * i + d];
+        if (pos[3 * i + d] > hi[d]) hi[d] = pos[3 * i + d];
+      }
+    for (int d = 0; d < 3; ++d) span[d] = hi[d] - lo[d];
+  }
+  int G[3];
+  int64_t ncell = 1;
+  for (int d = 0; d < 3; ++d) {
+    double g = floor(span[d] / w);
+    if (g < 1) g = 1;
+    if (g > 1024) g = 1024; /* coarser cells stay correct (width only grows) */
+    G[d] = (int)g;
+    ncell *= G[d];
+    if (dom.periodic && G[d] < 3) return oracle_fof_brute(pos, n, box, b2, label);
+  }
+  grid_t g;
+  g.start = (int64_t *)calloc((size_t)ncell + 1, sizeof(int64_t));
+  g.order = (int32_t *)malloc((size_t)(n > 0 ? n : 1) * sizeof(int32_t));
+  int32_t *cell = (int32_t *)malloc((size_t)(n > 0 ? n : 1) * sizeof(int32_t));
+  int64_t *fill = (int64_t *)malloc((size_t)ncell * sizeof(int64_t));
+  if (!g.start || !g.order || !cell || !fill) {
+    free(g.start);
+    free(g.order);
+    free(cell);
+    free(fill);
+    return 7;
+  }
+  for (int d = 0; d < 3; ++d) {
+    g.G[d] = G[d];
+    g.lo[d] = lo[d];
+    g.w[d] = span[d] > 0 ? span[d] / G[d] : 1.0;
+  }
+  for (int64_t i = 0; i < n; ++i) {
+    const float *p = pos + 3 * i;
+    int64_t c = ((int64_t)cell_coord(&g, p[0], 0) * G[1] + cell_coord(&g, p[1], 1)) * G[2] + cell_coord(&g, p[2], 2);
+    cell[i] = (int32_t)c;
+    g.start[c + 1]++;
+  }
+  for (int64_t c = 0; c < ncell; ++c) g.start[c + 1] += g.start[c];
+  memcpy(fill, g.start, (size_t)ncell * sizeof(int64_t));
+  for (int64_t i = 0; i < n; ++i) g.order[fill[cell[i]]++] = (int32_t)i;
+  for (int64_t i = 0; i < n; ++i) label[i] = (int32_t)i;
+  for (int64_t i = 0; i < n; ++i) {
+    const float *p = pos + 3 * i;
+    const int c0[3] = {cell_coord(&g, p[0], 0), cell_coord(&g, p[1], 1), cell_coord(&g, p[2], 2)};
+    for (int dx = -1; dx <= 1; ++dx)
+      for (int dy = -1; dy <= 1; ++dy)
+        for (int dz = -1; dz <= 1; ++dz) {
+          int cc[3] = {c0[0] + dx, c0[1] + dy, c0[2] + dz};
+          int skip = 0;
+          for (int d = 0; d < 3; ++d) {
+            if (cc[d] < 0 || cc[d] >= G[d]) {
+              if (dom.periodic)
+                cc[d] = (cc[d] + G[d]) % G[d];
+              else
+                skip = 1;
+            }
+          }
+          if (skip) continue;
+          const int64_t c = ((int64_t)cc[0] * G[1] + cc[1]) * G[2] + cc[2];
+          for (int64_t a = g.start[c]; a < g.start[c + 1]; ++a) {
+            const int32_t j = g.order[a];
+            if (j > i && canon_d2(p, pos + 3 * (int64_t)j, &dom) <= b2) uf_union(label, (int32_t)i, j);
+          }
+        }
+  }
+  uf_labels(label, n);
+  free(cell);
+  free(fill);
+  grid_free(&g);
+  return 0;
+}

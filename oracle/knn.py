@@ -53,6 +53,10 @@ def _load():
             lib.oracle_knn_grid_q.restype = ctypes.c_int
             lib.oracle_pair_d2.argtypes = [P, P, ctypes.c_int64, P, P]
             lib.oracle_pair_d2.restype = None
+            lib.oracle_fof_brute.argtypes = [P, ctypes.c_int64, P, ctypes.c_float, P]
+            lib.oracle_fof_brute.restype = ctypes.c_int
+            lib.oracle_fof_grid.argtypes = [P, ctypes.c_int64, P, ctypes.c_float, P]
+            lib.oracle_fof_grid.restype = ctypes.c_int
             lib.oracle_max_threads.argtypes = []
             lib.oracle_max_threads.restype = ctypes.c_int
             _lib = lib
@@ -126,3 +130,50 @@ def pair_d2(a, b, box=None):
     out = np.empty(a.shape[0], dtype=np.float32)
     _load().oracle_pair_d2(_ptr(a), _ptr(b), a.shape[0], _ptr(bx), _ptr(out))
     return out
+
+
+# ----------------------------------------------------------------------------- friends-of-friends
+def fof_b2(r_link) -> np.float32:
+    """The linking threshold on the canonical d2: RN32(r_link * r_link) (R21)."""
+    r = np.float32(r_link)
+    return np.float32(r * r)
+
+
+def fof_labels(pos, r_link, box=None, method: str = "grid"):
+    """PAPER.md §5 (L466-474): label[i] = smallest index of i's connected component of the graph
+    {i ~ j : canonical d2(p_i, p_j) <= RN32(r_link^2)}."""
+    pos, b = _prep(pos, box)
+    n = pos.shape[0]
+    lab = np.empty(n, dtype=np.int32)
+    fn = _load().oracle_fof_grid if method == "grid" else _load().oracle_fof_brute
+    rc = fn(_ptr(pos), n, _ptr(b), ctypes.c_float(fof_b2(r_link)), _ptr(lab))
+    if rc != 0:
+        raise ValueError(f"oracle fof returned status {rc}")
+    return lab
+
+
+def fof_catalogue(pos, labels, box=None, min_count: int = 20):
+    """PAPER.md L500-504 summary statistics of the groups with >= min_count points, ordered by
+    label (R22): (label int32, count int64, centre of mass float64 [g,3], inertia radius
+    float64 [g]). Positions are taken relative to the group's label point, as minimal images when
+    periodic; the centre of mass is wrapped into [0, L)."""
+    pos = np.asarray(pos, dtype=np.float32).astype(np.float64)
+    labels = np.asarray(labels)
+    u, cnt = np.unique(labels, return_counts=True)
+    keep = cnt >= min_count
+    u, cnt = u[keep], cnt[keep]
+    L = None if box is None else np.broadcast_to(np.asarray(box, np.float64), (3,))
+    com = np.empty((len(u), 3))
+    rad = np.empty(len(u))
+    for gi, g in enumerate(u):
+        m = pos[labels == g]
+        disp = m - pos[g]
+        if L is not None:
+            disp = disp - L * np.round(disp / L)
+        mean = disp.mean(axis=0)
+        c = pos[g] + mean
+        if L is not None:
+            c = c - L * np.floor(c / L)
+        com[gi] = c
+        rad[gi] = np.sqrt(((disp - mean) ** 2).sum(axis=1).mean())
+    return u.astype(np.int32), cnt.astype(np.int64), com, rad
