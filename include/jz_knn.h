@@ -215,6 +215,25 @@ JZ_API int jz_knn_select_ghosts(jz_knn_index *ix, const float *boxes, int64_t nb
 JZ_API int jz_knn_pack_ghosts(jz_knn_index *ix, const int32_t *mask, int32_t nranks, const int64_t *offsets, float *out4,
                        jz_stream_t s);
 
+/* F4 -- friends-of-friends (§5) on an index built over points that are both
+ * sources and queries (jz_knn_build; JZ_EINVAL otherwise). Groups are the connected components
+ * of the graph with an edge between two points iff their canonical FP32 d2 (as for kNN) is
+ * <= RN32(r_link * r_link) (R21). The walk is the kNN dual walk with a fixed radius;
+ * links go to a union-find over z positions with atomic compare-and-swap.
+ *   labels [n] int32 (device, caller-owned): label of input row i = the smallest input index of
+ *          its group (unique, so bit-comparable).
+ *   *ngroups (host, may be NULL): number of groups with >= min_count points (paper 20).
+ * The catalogue of those groups stays in the index until the next jz_fof / jz_knn_free.
+ * Synchronises s. */
+JZ_API int jz_fof(jz_knn_index *ix, float r_link, int32_t min_count, int32_t *labels, int64_t *ngroups, jz_stream_t s);
+/* Copy the catalogue (device arrays of >= ngroups entries; JZ_ECAPACITY if cap < ngroups), in the
+ * paper's group order (z order of each group's first point): label int32, count int32,
+ * centre of mass float64 [g][3] (periodic: wrapped into [0, L)), inertia radius float64 (rms
+ * distance to the centre). FP64 sums in nondeterministic order: last-bit differences between
+ * runs. */
+JZ_API int jz_fof_catalogue(const jz_knn_index *ix, int64_t cap, int32_t *label, int32_t *count, double *com,
+                            double *rad, jz_stream_t s);
+
 /* F2 -- multi-GPU rows in input order ("final reordering step": the
  * reverse all-to-all of the result). Step 1 (sender): the z-ordered rows of this rank
  * (idx [m][k] int32, d2 [m][k] float32, row_gidx [m] int32, from jz_knn_query with

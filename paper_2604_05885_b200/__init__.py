@@ -87,6 +87,25 @@ class KnnIndex:
                                        B.dptr(rg) if rg is not None else None, B.stream_ptr(self.stream)))
         return (idx, d2) if o == B.JZ_ORDER_INPUT else (idx, d2, rg)
 
+    def fof(self, r_link: float, min_count: int = 20, labels=None):
+        """Friends-of-friends (§5): (labels int32 [n] in input order = smallest
+        input index of each point's group, catalogue dict of the groups with >= min_count points
+        in the paper's group order: label, count, com [g,3] float64, rad float64)."""
+        if labels is None:
+            labels = torch.empty((self.n,), dtype=torch.int32, device=self.device)
+        ng = ctypes.c_int64()
+        st = B.stream_ptr(self.stream)
+        B.check(self._lib.jz_fof(self._h, float(r_link), int(min_count), B.dptr(labels), ctypes.byref(ng), st))
+        g = ng.value
+        cat = {"label": torch.empty((g,), dtype=torch.int32, device=self.device),
+               "count": torch.empty((g,), dtype=torch.int32, device=self.device),
+               "com": torch.empty((g, 3), dtype=torch.float64, device=self.device),
+               "rad": torch.empty((g,), dtype=torch.float64, device=self.device)}
+        if g:
+            B.check(self._lib.jz_fof_catalogue(self._h, g, B.dptr(cat["label"]), B.dptr(cat["count"]),
+                                               B.dptr(cat["com"]), B.dptr(cat["rad"]), st))
+        return labels, cat
+
     def stage_times(self):
         """Per-phase device ms of the last build + query (needs set_timing(True) before the build)."""
         t = (ctypes.c_float * 6)()
@@ -150,6 +169,15 @@ def knn(pos: torch.Tensor, k: int, box=None, order: str = "input", params=None, 
     ix = KnnIndex(pos, box=box, params=params, stream=stream, queries=queries)
     try:
         return ix.query(k, order=order)
+    finally:
+        ix.free()
+
+
+def fof(pos: torch.Tensor, r_link: float, box=None, min_count: int = 20, params=None, stream=None):
+    """One-shot friends-of-friends (build + jz_fof): (labels, catalogue), see KnnIndex.fof."""
+    ix = KnnIndex(pos, box=box, params=params, stream=stream)
+    try:
+        return ix.fof(r_link, min_count)
     finally:
         ix.free()
 

@@ -22,6 +22,7 @@ EXPORTS = [
     "jz_knn_stage_times", "jz_set_timing", "jz_last_error", "jz_morton_keys", "jz_bucket_by_splitters",
     "jz_pack_by_rank", "jz_knn_plane_nodes", "jz_knn_query_boxes", "jz_knn_select_ghosts", "jz_knn_pack_ghosts",
     "jz_knn_debug_copy", "jz_launch_count", "jz_knn_stats", "jz_pack_rows", "jz_scatter_rows",
+    "jz_fof", "jz_fof_catalogue",
 ]
 
 
@@ -80,6 +81,8 @@ def lib():
             "jz_knn_stats": ([P, P], ctypes.c_int),
             "jz_pack_rows": ([P, P, P, I64, I32, P, P, I32, P, P], ctypes.c_int),
             "jz_scatter_rows": ([P, I64, I32, I64, I64, P, P, P], ctypes.c_int),
+            "jz_fof": ([P, ctypes.c_float, I32, P, P, P], ctypes.c_int),
+            "jz_fof_catalogue": ([P, I64, P, P, P, P, P], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)

@@ -25,6 +25,7 @@ struct jz_knn_index {
   float4 *spts = nullptr, *qpts = nullptr;
   int32_t *sbeg = nullptr, *qbeg = nullptr, *qin = nullptr;
   bool own_s = false, own_q = false;
+  bool input_ids = false;  // point ids are input positions 0..n-1 (jz_knn_build): needed by jz_fof
   std::vector<jz::Plane> planes;
   cudaEvent_t ev[8] = {};
   bool timing = false;
@@ -32,6 +33,10 @@ struct jz_knn_index {
   long long evals = 0, inserts = 0;
   long long walk[5] = {0, 0, 0, 0, 0};  // entries, warp-passed leaves, staged leaves, flush rounds, work items
   unsigned long long *d_evals = nullptr;
+  // friends-of-friends catalogue of the last jz_fof call (device; group order = root z-order)
+  int64_t fof_ngroups = 0;
+  int32_t *fof_label = nullptr, *fof_count = nullptr;
+  double *fof_com = nullptr, *fof_rad = nullptr;
 };
 
 #include <atomic>
@@ -197,6 +202,87 @@ void split_types(jz_knn_index *ix, bool typed) {
   JZ_CUDA(cudaFreeAsync(qr, st));
 }
 
+// ---- friends-of-friends (§5)
+__global__ void k_fof_init(int32_t *__restrict__ par, int32_t *__restrict__ minlab, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    par[i] = (int32_t)i;
+    minlab[i] = INT32_MAX;
+  }
+}
+// contraction ("setting every pointer to its root"): runs after every link is done
+__global__ void k_fof_flatten(int32_t *__restrict__ par, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t x = par[i];
+    while (par[x] != x) x = par[x];
+    par[i] = x;
+  }
+}
+__global__ void k_fof_minlab(const float4 *__restrict__ pts, const int32_t *__restrict__ par, int64_t n,
+                             int32_t *__restrict__ minlab) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    atomicMin(&minlab[par[i]], __float_as_int(pts[i].w));
+}
+// label of input row gidx = smallest input index of its group (R21)
+__global__ void k_fof_labels(const float4 *__restrict__ pts, const int32_t *__restrict__ par,
+                             const int32_t *__restrict__ minlab, int64_t n, int32_t *__restrict__ labels) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    labels[__float_as_int(pts[i].w)] = minlab[par[i]];
+}
+__device__ __forceinline__ double fof_disp(float x, float xr, int periodic, float L) {
+  double d = (double)x - (double)xr;
+  if (periodic) d -= (double)L * rint(d / (double)L);  // minimal image w.r.t. the group's root point
+  return d;
+}
+__global__ void k_fof_sum1(const float4 *__restrict__ pts, const int32_t *__restrict__ par, int64_t n, jz::Dom D,
+                           int32_t *__restrict__ cnt, double *__restrict__ sum) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t r = par[i];
+    const float4 p = pts[i], q = pts[r];
+    atomicAdd(&cnt[r], 1);
+    atomicAdd(&sum[3 * (int64_t)r + 0], fof_disp(p.x, q.x, D.periodic, D.L[0]));
+    atomicAdd(&sum[3 * (int64_t)r + 1], fof_disp(p.y, q.y, D.periodic, D.L[1]));
+    atomicAdd(&sum[3 * (int64_t)r + 2], fof_disp(p.z, q.z, D.periodic, D.L[2]));
+  }
+}
+__global__ void k_fof_sum2(const float4 *__restrict__ pts, const int32_t *__restrict__ par, int64_t n, jz::Dom D,
+                           const int32_t *__restrict__ cnt, const double *__restrict__ sum, double *__restrict__ ss) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t r = par[i];
+    const float4 p = pts[i], q = pts[r];
+    const double c = (double)cnt[r];
+    const double dx = fof_disp(p.x, q.x, D.periodic, D.L[0]) - sum[3 * (int64_t)r] / c;
+    const double dy = fof_disp(p.y, q.y, D.periodic, D.L[1]) - sum[3 * (int64_t)r + 1] / c;
+    const double dz = fof_disp(p.z, q.z, D.periodic, D.L[2]) - sum[3 * (int64_t)r + 2] / c;
+    atomicAdd(&ss[r], dx * dx + dy * dy + dz * dz);
+  }
+}
+__global__ void k_fof_flags(const int32_t *__restrict__ par, const int32_t *__restrict__ cnt, int64_t n, int min_count,
+                            int32_t *__restrict__ flag) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    flag[i] = par[i] == (int32_t)i && cnt[i] >= min_count;
+}
+__global__ void k_fof_cat(const float4 *__restrict__ pts, const int32_t *__restrict__ flag,
+                          const int64_t *__restrict__ pos, const int32_t *__restrict__ minlab,
+                          const int32_t *__restrict__ cnt, const double *__restrict__ sum,
+                          const double *__restrict__ ss, int64_t n, jz::Dom D, int32_t *__restrict__ olab,
+                          int32_t *__restrict__ ocnt, double *__restrict__ ocom, double *__restrict__ orad) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+    if (!flag[r]) continue;
+    const int64_t o = pos[r];
+    const double c = (double)cnt[r];
+    const float4 q = pts[r];
+    const float qq[3] = {q.x, q.y, q.z};
+    for (int d = 0; d < 3; ++d) {
+      double v = (double)qq[d] + sum[3 * r + d] / c;
+      if (D.periodic) v -= (double)D.L[d] * floor(v / (double)D.L[d]);  // wrapped into [0, L)
+      ocom[3 * o + d] = v;
+    }
+    olab[o] = minlab[r];
+    ocnt[o] = cnt[r];
+    orad[o] = sqrt(ss[r] / c);
+  }
+}
+
 jz_knn_index *build_impl(const float *pos, int64_t n, int stride, int gidx_mode, int64_t n_query, const float *box,
                          const jz_knn_params *p, cudaStream_t st) {
   if (!pos) throw jz::Error(JZ_EINVAL, "pos is NULL");
@@ -215,6 +301,7 @@ jz_knn_index *build_impl(const float *pos, int64_t n, int stride, int gidx_mode,
   ix->n_query = n_query;
   ix->D = make_dom(box);
   ix->prm = prm;
+  ix->input_ids = gidx_mode == 0;
   ix->timing = timing_enabled();
   try {
     if (ix->timing)
@@ -396,6 +483,10 @@ void jz_knn_free(jz_knn_index *ix) {
   if (ix->keys) cudaFreeAsync(ix->keys, st);
   if (ix->perm) cudaFreeAsync(ix->perm, st);
   if (ix->d_evals) cudaFreeAsync(ix->d_evals, st);
+  if (ix->fof_label) cudaFreeAsync(ix->fof_label, st);
+  if (ix->fof_count) cudaFreeAsync(ix->fof_count, st);
+  if (ix->fof_com) cudaFreeAsync(ix->fof_com, st);
+  if (ix->fof_rad) cudaFreeAsync(ix->fof_rad, st);
   cudaStreamSynchronize(st);
   for (auto &e : ix->ev)
     if (e) cudaEventDestroy(e);
@@ -434,6 +525,122 @@ int jz_knn_search_host(const float *pos_host, int64_t n, const float *box, const
   JZ_CUDA(cudaFreeAsync(dd2, st));
   JZ_CUDA(cudaStreamSynchronize(st));
   return rc;
+  JZ_API_END
+}
+
+int jz_fof(jz_knn_index *ix, float r_link, int32_t min_count, int32_t *labels, int64_t *ngroups, jz_stream_t s) {
+  JZ_API_BEGIN
+  if (!ix || !labels) return fail(JZ_EINVAL, "NULL argument");
+  if (!(r_link >= 0.f) || !std::isfinite(r_link)) return fail(JZ_EINVAL, "r_link must be finite and >= 0");
+  if (min_count < 1) return fail(JZ_EINVAL, "min_count must be >= 1");
+  if (ix->n_query != ix->n || ix->n_src != ix->n || !ix->input_ids)
+    return fail(JZ_EINVAL, "friends-of-friends needs an index built by jz_knn_build (every point a source and a query)");
+  cudaStream_t st = (cudaStream_t)s;
+  ix->st = st;
+  const int64_t n = ix->n;
+  const float b2 = r_link * r_link;  // RN32(r_link^2): the threshold on the canonical d2 (R21)
+  rec(ix, 4);
+  jz::IList il;
+  float *rmax2 = nullptr;
+  int32_t *superbeg = nullptr;
+  jz::walk_to(ix->planes, ix->D, 1, ix->prm.ngr, ix->prm.flags, 1, il, &rmax2, &superbeg, st, b2);
+  rec(ix, 5);
+  int32_t *par = nullptr, *minlab = nullptr, *cnt = nullptr, *flag = nullptr;
+  double *sum = nullptr, *ss = nullptr;
+  int64_t *pos = nullptr;
+  JZ_CUDA(cudaMallocAsync(&par, n * sizeof(int32_t), st));
+  JZ_CUDA(cudaMallocAsync(&minlab, n * sizeof(int32_t), st));
+  k_fof_init<<<jz::grid_for(n, 256), 256, 0, st>>>(par, minlab, n);
+  JZ_LAUNCH_CHECK();
+  if (!ix->d_evals) JZ_CUDA(cudaMallocAsync(&ix->d_evals, 16 * sizeof(unsigned long long), st));
+  JZ_CUDA(cudaMemsetAsync(ix->d_evals, 0, 16 * sizeof(unsigned long long), st));
+  const bool one_plane = ix->planes.size() == 1;
+  jz::LeafArgs la{};
+  la.spts = ix->pts;
+  la.sbeg = ix->planes[0].beg;
+  la.qpts = ix->pts;
+  la.qbeg = ix->planes[0].beg;
+  la.qin = ix->perm;
+  la.leaf_box = ix->planes[0].box;
+  la.nleaf = ix->planes[0].nnodes;
+  la.par_leaf = one_plane ? superbeg : ix->planes[1].beg;
+  la.par_box = one_plane ? nullptr : ix->planes[1].box;
+  la.npar = il.nrecv;
+  la.il = &il;
+  la.flags = ix->prm.flags;
+  la.evals = ix->d_evals;
+  jz::fof_leaf(la, ix->D, b2, par, st);
+  k_fof_flatten<<<jz::grid_for(n, 256), 256, 0, st>>>(par, n);
+  JZ_LAUNCH_CHECK();
+  k_fof_minlab<<<jz::grid_for(n, 256), 256, 0, st>>>(ix->pts, par, n, minlab);
+  JZ_LAUNCH_CHECK();
+  k_fof_labels<<<jz::grid_for(n, 256), 256, 0, st>>>(ix->pts, par, minlab, n, labels);
+  JZ_LAUNCH_CHECK();
+  // catalogue: groups with >= min_count points, in root z-order (the paper's group order)
+  JZ_CUDA(cudaMallocAsync(&cnt, n * sizeof(int32_t), st));
+  JZ_CUDA(cudaMallocAsync(&sum, 3 * n * sizeof(double), st));
+  JZ_CUDA(cudaMallocAsync(&ss, n * sizeof(double), st));
+  JZ_CUDA(cudaMallocAsync(&flag, n * sizeof(int32_t), st));
+  JZ_CUDA(cudaMallocAsync(&pos, (n + 1) * sizeof(int64_t), st));
+  JZ_CUDA(cudaMemsetAsync(cnt, 0, n * sizeof(int32_t), st));
+  JZ_CUDA(cudaMemsetAsync(sum, 0, 3 * n * sizeof(double), st));
+  JZ_CUDA(cudaMemsetAsync(ss, 0, n * sizeof(double), st));
+  k_fof_sum1<<<jz::grid_for(n, 256), 256, 0, st>>>(ix->pts, par, n, ix->D, cnt, sum);
+  JZ_LAUNCH_CHECK();
+  k_fof_sum2<<<jz::grid_for(n, 256), 256, 0, st>>>(ix->pts, par, n, ix->D, cnt, sum, ss);
+  JZ_LAUNCH_CHECK();
+  k_fof_flags<<<jz::grid_for(n, 256), 256, 0, st>>>(par, cnt, n, min_count, flag);
+  JZ_LAUNCH_CHECK();
+  jz::exclusive_scan_i32_to_i64(flag, pos, n, st);
+  const int64_t ng = jz::read_i64(pos + n, st);
+  if (ix->fof_label) JZ_CUDA(cudaFreeAsync(ix->fof_label, st));
+  if (ix->fof_count) JZ_CUDA(cudaFreeAsync(ix->fof_count, st));
+  if (ix->fof_com) JZ_CUDA(cudaFreeAsync(ix->fof_com, st));
+  if (ix->fof_rad) JZ_CUDA(cudaFreeAsync(ix->fof_rad, st));
+  const int64_t ga = ng > 0 ? ng : 1;
+  JZ_CUDA(cudaMallocAsync(&ix->fof_label, ga * sizeof(int32_t), st));
+  JZ_CUDA(cudaMallocAsync(&ix->fof_count, ga * sizeof(int32_t), st));
+  JZ_CUDA(cudaMallocAsync(&ix->fof_com, 3 * ga * sizeof(double), st));
+  JZ_CUDA(cudaMallocAsync(&ix->fof_rad, ga * sizeof(double), st));
+  k_fof_cat<<<jz::grid_for(n, 256), 256, 0, st>>>(ix->pts, flag, pos, minlab, cnt, sum, ss, n, ix->D, ix->fof_label,
+                                                  ix->fof_count, ix->fof_com, ix->fof_rad);
+  JZ_LAUNCH_CHECK();
+  ix->fof_ngroups = ng;
+  rec(ix, 6);
+  il.release(st);
+  if (rmax2) JZ_CUDA(cudaFreeAsync(rmax2, st));
+  if (superbeg) JZ_CUDA(cudaFreeAsync(superbeg, st));
+  for (void *p : {(void *)par, (void *)minlab, (void *)cnt, (void *)sum, (void *)ss, (void *)flag, (void *)pos})
+    JZ_CUDA(cudaFreeAsync(p, st));
+  unsigned long long ev = 0;
+  JZ_CUDA(cudaMemcpyAsync(&ev, ix->d_evals, sizeof(ev), cudaMemcpyDeviceToHost, st));
+  JZ_CUDA(cudaStreamSynchronize(st));
+  ix->evals = (long long)ev;
+  if (ix->timing) {
+    cudaEventElapsedTime(&ix->times[3], ix->ev[4], ix->ev[5]);
+    cudaEventElapsedTime(&ix->times[4], ix->ev[5], ix->ev[6]);
+    ix->times[5] = ix->times[0] + ix->times[1] + ix->times[2] + ix->times[3] + ix->times[4];
+  }
+  if (ngroups) *ngroups = ng;
+  return JZ_OK;
+  JZ_API_END
+}
+
+int jz_fof_catalogue(const jz_knn_index *ix, int64_t cap, int32_t *label, int32_t *count, double *com, double *rad,
+                     jz_stream_t s) {
+  JZ_API_BEGIN
+  if (!ix) return fail(JZ_EINVAL, "NULL index");
+  const int64_t ng = ix->fof_ngroups;
+  if (cap < ng) return fail(JZ_ECAPACITY, "catalogue capacity below the number of groups");
+  if (ng > 0 && (!label || !count || !com || !rad)) return fail(JZ_EINVAL, "NULL argument");
+  cudaStream_t st = (cudaStream_t)s;
+  if (ng > 0) {
+    JZ_CUDA(cudaMemcpyAsync(label, ix->fof_label, ng * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+    JZ_CUDA(cudaMemcpyAsync(count, ix->fof_count, ng * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+    JZ_CUDA(cudaMemcpyAsync(com, ix->fof_com, 3 * ng * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    JZ_CUDA(cudaMemcpyAsync(rad, ix->fof_rad, ng * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  }
+  return JZ_OK;
   JZ_API_END
 }
 

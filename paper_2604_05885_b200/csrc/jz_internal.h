@@ -55,8 +55,10 @@ struct IList {
 // one-plane tree and stop = 1), the receivers are the super nodes: *superbeg (first top
 // node of each super node, caller frees) is set, the list is the dense one and
 // *rmax2 = nullptr (= +inf).
+// fixed_r2 >= 0: fixed-radius walk (friends-of-friends): no FindRmax, every node's radius^2 is
+// fixed_r2, so the lists hold the pairs with d_low^2 <= fixed_r2.
 void walk_to(const std::vector<Plane> &planes, const Dom &D, int k, int ngr, unsigned flags, int stop, IList &il,
-             float **rmax2, int32_t **superbeg, cudaStream_t st);
+             float **rmax2, int32_t **superbeg, cudaStream_t st, float fixed_r2 = -1.f);
 
 // leaf-to-leaf (jz_leaf.cu)
 struct LeafArgs {
@@ -81,6 +83,10 @@ struct LeafArgs {
   unsigned long long *evals;  // device counter (may be nullptr)
 };
 void leaf_to_leaf(const LeafArgs &a, const Dom &D, cudaStream_t st);
+
+// friends-of-friends leaf stage (jz_leaf.cu): links every pair of points with canonical
+// d2 <= b2 in the union-find array par (sorted positions; roots = smallest position)
+void fof_leaf(const LeafArgs &a, const Dom &D, float b2, int32_t *par, cudaStream_t st);
 
 // read-only view of an index for the multi-GPU stage kernels (jz_dist.cu)
 struct IndexView {

@@ -827,6 +827,281 @@ __global__ void __launch_bounds__(kLThreads, JZ_MINB) k_leaf(LeafPK a, Dom D) {
   }
 }
 
+// ---------------------------------------------------------------- friends-of-friends (F4)
+// PAPER.md §5 (L466-474, L488-490): every pair of points with canonical d2 <= b2 is linked in a
+// union-find over sorted positions; a link hangs the larger root under the smaller one with an
+// atomic compare-and-swap and retries on failure, so a root is its component's smallest
+// position. The walk is the kNN one with a fixed radius: the same 32-query work items, own
+// pre-pass, plane-1 interaction lists (d_low^2 <= b2), per-leaf warp-box and per-lane tests, packed
+// FP32 distances. Each unordered pair is linked from its lower-positioned point only.
+struct FofBuf {
+  float x[kLCap + 8], y[kLCap + 8], z[kLCap + 8];
+  int g[kLCap + 8];  // sorted position of the staged source
+};
+
+// root of x with path halving (x only ever points to one of its ancestors, so the plain
+// stores are benign under concurrent unions); L2 loads: other SMs link concurrently
+__device__ __forceinline__ int fof_find(int32_t *par, int x) {
+  while (true) {
+    const int p = __ldcg(&par[x]);
+    if (p == x) return x;
+    const int pp = __ldcg(&par[p]);
+    if (pp == p) return p;
+    __stcg(&par[x], pp);
+    x = pp;
+  }
+}
+
+__device__ __forceinline__ void fof_union(int32_t *par, int a, int b) {
+  while (true) {
+    a = fof_find(par, a);
+    b = fof_find(par, b);
+    if (a == b) return;
+    if (a > b) {
+      const int t = a;
+      a = b;
+      b = t;
+    }
+    const int old = atomicCAS(&par[b], b, a);  // hang the larger root under the smaller one
+    if (old == b) return;
+    b = old;  // b stopped being a root: retry from its new parent
+  }
+}
+
+struct FofPK {
+  const float4 *spts;
+  const int32_t *sbeg;
+  const CE *leaf_ce;
+  const int32_t *par_leaf;
+  const CE *par_ce;
+  const int64_t *ispl;
+  const int32_t *isrc;
+  const float *rlow;
+  const int32_t *item_par;
+  const int32_t *item_q0;
+  int64_t nitems;
+  float b2;
+  float Lmax;
+  int sorted;
+  int32_t *par;
+  unsigned long long *stats;  // [0] distance evaluations
+};
+
+// staged sources [0, n) (n multiple of 8) against the lane's query qi
+template <bool PER>
+__device__ __forceinline__ void fof_eval(FofBuf &B, int n, int qi, float qx, float qy, float qz, bool shift, float shx,
+                                         float shy, float shz, bool generic, const Dom &D, float b2, int32_t *par,
+                                         bool act) {
+  const u64 QX = pk(qx, qx), QY = pk(qy, qy), QZ = pk(qz, qz);
+  const u64 SX = pk(shx, shx), SY = pk(shy, shy), SZ = pk(shz, shz);
+#pragma unroll 1
+  for (int j = 0; j < n; j += 8) {
+    float a0, a1, a2, a3, b0, b1, b2v, b3;
+    if (!PER || !generic) {
+      d2x4(B.x, B.y, B.z, j, QX, QY, QZ, shift, SX, SY, SZ, a0, a1, a2, a3);
+      d2x4(B.x, B.y, B.z, j + 4, QX, QY, QZ, shift, SX, SY, SZ, b0, b1, b2v, b3);
+    } else {  // straddling pair: per-pair minimal image (canonical select)
+      a0 = canon_d2_per(qx, qy, qz, B.x[j], B.y[j], B.z[j], D);
+      a1 = canon_d2_per(qx, qy, qz, B.x[j + 1], B.y[j + 1], B.z[j + 1], D);
+      a2 = canon_d2_per(qx, qy, qz, B.x[j + 2], B.y[j + 2], B.z[j + 2], D);
+      a3 = canon_d2_per(qx, qy, qz, B.x[j + 3], B.y[j + 3], B.z[j + 3], D);
+      b0 = canon_d2_per(qx, qy, qz, B.x[j + 4], B.y[j + 4], B.z[j + 4], D);
+      b1 = canon_d2_per(qx, qy, qz, B.x[j + 5], B.y[j + 5], B.z[j + 5], D);
+      b2v = canon_d2_per(qx, qy, qz, B.x[j + 6], B.y[j + 6], B.z[j + 6], D);
+      b3 = canon_d2_per(qx, qy, qz, B.x[j + 7], B.y[j + 7], B.z[j + 7], D);
+    }
+    const float m = fminf(fminf(fminf(a0, a1), fminf(a2, a3)), fminf(fminf(b0, b1), fminf(b2v, b3)));  // NaN ignored
+    if (__any_sync(0xffffffffu, act && m <= b2)) {
+      unsigned mk = act ? ((a0 <= b2) | ((a1 <= b2) << 1) | ((a2 <= b2) << 2) | ((a3 <= b2) << 3) | ((b0 <= b2) << 4) |
+                           ((b1 <= b2) << 5) | ((b2v <= b2) << 6) | ((b3 <= b2) << 7))
+                        : 0u;
+      while (mk) {  // one inlined union site
+        const int i = __ffs(mk) - 1;
+        mk &= mk - 1;
+        const int g = B.g[j + i];
+        if (g > qi) fof_union(par, qi, g);
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ int fof_pad8(FofBuf &B, int n) {
+  const int lane = threadIdx.x & 31;
+  if (n & 4) {
+    if (lane < 4) {
+      const float nan = __int_as_float(0x7fc00000);
+      B.x[n + lane] = nan;
+      B.y[n + lane] = nan;
+      B.z[n + lane] = nan;
+      B.g[n + lane] = -1;
+    }
+    n += 4;
+  }
+  return n;
+}
+
+template <bool PER>
+__global__ void __launch_bounds__(kLThreads, 12) k_fof_leaf(FofPK a, Dom D) {
+  __shared__ __align__(16) FofBuf s_buf[kLWarps];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t item = (int64_t)blockIdx.x * kLWarps + warp;
+  if (item >= a.nitems) return;
+  FofBuf &B = s_buf[warp];
+  const int J = a.item_par[item];
+  const int LJa = a.par_leaf[J], LJb = a.par_leaf[J + 1];
+  const int qhi = a.sbeg[LJb];
+  const int q0 = a.item_q0[item];
+  const int qi = q0 + lane;
+  const bool act = qi < qhi;
+  float qx = 0.f, qy = 0.f, qz = 0.f;
+  if (act) {
+    const float4 q = a.spts[qi];
+    qx = q.x;
+    qy = q.y;
+    qz = q.z;
+  }
+  float blo[3] = {act ? qx : INFINITY, act ? qy : INFINITY, act ? qz : INFINITY};
+  float bhi[3] = {act ? qx : -INFINITY, act ? qy : -INFINITY, act ? qz : -INFINITY};
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      blo[d] = fminf(blo[d], __shfl_xor_sync(0xffffffffu, blo[d], o));
+      bhi[d] = fmaxf(bhi[d], __shfl_xor_sync(0xffffffffu, bhi[d], o));
+    }
+  }
+  const CE wb = make_ce(blo[0], blo[1], blo[2], bhi[0], bhi[1], bhi[2], a.Lmax);
+  const float b2 = a.b2;
+  unsigned long long nev = 0;
+  // own leaves [xa, xb): their sources are contiguous; every pair inside is a candidate
+  int xa = 0x7fffffff, xb = -1;
+  {
+    const int qend = min(q0 + 32, qhi);
+    for (int l0 = LJa; l0 < LJb; l0 += 32) {
+      const int l = l0 + lane;
+      const bool ov = l < LJb && a.sbeg[l] < qend && a.sbeg[l + 1] > q0;
+      const unsigned b = __ballot_sync(0xffffffffu, ov);
+      if (b) {
+        xa = min(xa, l0 + __ffs(b) - 1);
+        xb = max(xb, l0 + 32 - __clz(b));
+      }
+    }
+    int cls_all = 0;
+    if (PER) {
+      for (int l = xa + lane; l < xb; l += 32) {
+        const CE lc = a.leaf_ce[l];
+        cls_all |= ce_class(__fsub_rn(wb.c.x, lc.c.x), __fadd_ru(wb.e.x, lc.e.x), D.h[0]) |
+                   ce_class(__fsub_rn(wb.c.y, lc.c.y), __fadd_ru(wb.e.y, lc.e.y), D.h[1]) |
+                   ce_class(__fsub_rn(wb.c.z, lc.c.z), __fadd_ru(wb.e.z, lc.e.z), D.h[2]);
+      }
+      cls_all = __reduce_or_sync(0xffffffffu, cls_all);
+    }
+    const int s0 = a.sbeg[xa], s1 = a.sbeg[xb];
+    for (int b0 = max(s0, q0 + 1); b0 < s1; b0 += kLCap) {  // only sources after the warp's first query
+      const int m = min(kLCap, s1 - b0), mp = (m + 3) & ~3;
+      for (int t = lane; t < mp; t += 32) {
+        float4 p = make_float4(__int_as_float(0x7fc00000), __int_as_float(0x7fc00000), __int_as_float(0x7fc00000), 0.f);
+        if (t < m) p = a.spts[b0 + t];
+        B.x[t] = p.x;
+        B.y[t] = p.y;
+        B.z[t] = p.z;
+        B.g[t] = t < m ? b0 + t : -1;
+      }
+      nev += act ? (unsigned)m : 0u;
+      const int np = fof_pad8(B, mp);
+      __syncwarp();
+      fof_eval<PER>(B, np, qi, qx, qy, qz, false, 0.f, 0.f, 0.f, PER && cls_all != 0, D, b2, a.par, act);
+      __syncwarp();
+    }
+  }
+  const int64_t eb = a.ispl[J], ee = a.ispl[J + 1];
+  for (int64_t e = eb; e < ee; ++e) {
+    if (a.rlow[e] > b2) {
+      if (a.sorted) break;
+      continue;
+    }
+    const int S = a.isrc[e];
+    if (a.par_ce) {
+      const CE pc = a.par_ce[S];
+      if (dlow2_ce<PER>(__fsub_rn(wb.c.x, pc.c.x), __fsub_rn(wb.c.y, pc.c.y), __fsub_rn(wb.c.z, pc.c.z),
+                        __fadd_ru(wb.e.x, pc.e.x), __fadd_ru(wb.e.y, pc.e.y), __fadd_ru(wb.e.z, pc.e.z), D) > b2)
+        continue;
+    }
+    const int la = a.par_leaf[S], lb = a.par_leaf[S + 1];
+    const int ya = S == J ? xa : 0, yb = S == J ? xb : 0;
+    for (int l0 = la; l0 < lb; l0 += 32) {
+      const int l = l0 + lane;
+      bool pass = false;
+      int cls = 0, s0 = 0, s1 = 0;
+      float cx = 0.f, cy = 0.f, cz = 0.f, ex = 0.f, ey = 0.f, ez = 0.f;
+      if (l < lb && (l < ya || l >= yb)) {
+        const CE lc = a.leaf_ce[l];
+        cx = lc.c.x;
+        cy = lc.c.y;
+        cz = lc.c.z;
+        ex = lc.e.x;
+        ey = lc.e.y;
+        ez = lc.e.z;
+        const float dcx = __fsub_rn(wb.c.x, cx), dcy = __fsub_rn(wb.c.y, cy), dcz = __fsub_rn(wb.c.z, cz);
+        const float Ex = __fadd_ru(wb.e.x, ex), Ey = __fadd_ru(wb.e.y, ey), Ez = __fadd_ru(wb.e.z, ez);
+        s0 = a.sbeg[l];
+        s1 = a.sbeg[l + 1];
+        pass = s1 > q0 + 1 && dlow2_ce<PER>(dcx, dcy, dcz, Ex, Ey, Ez, D) <= b2;  // a source after some query
+        if (PER && pass)
+          cls = ce_class(dcx, Ex, D.h[0]) | (ce_class(dcy, Ey, D.h[1]) << 2) | (ce_class(dcz, Ez, D.h[2]) << 4);
+      }
+      unsigned bal = __ballot_sync(0xffffffffu, pass);
+      while (bal) {
+        const int c0 = __shfl_sync(0xffffffffu, cls, __ffs(bal) - 1);
+        int n = 0;
+        while (bal) {
+          const int src = __ffs(bal) - 1;
+          if (__shfl_sync(0xffffffffu, cls, src) != c0) break;
+          {
+            const float lcx = __shfl_sync(0xffffffffu, cx, src), lcy = __shfl_sync(0xffffffffu, cy, src),
+                        lcz = __shfl_sync(0xffffffffu, cz, src);
+            const float lex = __shfl_sync(0xffffffffu, ex, src), ley = __shfl_sync(0xffffffffu, ey, src),
+                        lez = __shfl_sync(0xffffffffu, ez, src);
+            const float dl =
+                dlow2_ce<PER>(__fsub_rn(qx, lcx), __fsub_rn(qy, lcy), __fsub_rn(qz, lcz), lex, ley, lez, D);
+            if (!__any_sync(0xffffffffu, act && dl <= b2)) {
+              bal &= bal - 1;
+              continue;
+            }
+          }
+          const int lp = __shfl_sync(0xffffffffu, s0, src), m = __shfl_sync(0xffffffffu, s1, src) - lp;
+          if (n + ((m + 3) & ~3) > kLCap) break;
+          bal &= bal - 1;
+          for (int t = lane; t < ((m + 3) & ~3); t += 32) {
+            float4 p = make_float4(__int_as_float(0x7fc00000), __int_as_float(0x7fc00000), __int_as_float(0x7fc00000),
+                                   0.f);
+            if (t < m) p = a.spts[lp + t];
+            B.x[n + t] = p.x;
+            B.y[n + t] = p.y;
+            B.z[n + t] = p.z;
+            B.g[n + t] = t < m ? lp + t : -1;
+          }
+          nev += act ? (unsigned)m : 0u;
+          n += (m + 3) & ~3;
+        }
+        if (n == 0) continue;
+        n = fof_pad8(B, n);
+        __syncwarp();
+        fof_eval<PER>(B, n, qi, qx, qy, qz, PER && c0 != 0, class_shift(c0 & 3, D.L[0]),
+                      class_shift((c0 >> 2) & 3, D.L[1]), class_shift((c0 >> 4) & 3, D.L[2]), PER && any_straddle(c0),
+                      D, b2, a.par, act);
+        __syncwarp();
+      }
+    }
+  }
+  if (a.stats) {
+    unsigned long long tot = nev;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    if (lane == 0) atomicAdd(&a.stats[0], tot);
+  }
+}
+
 // work items: 32-query groups of each receiving parent, in z order
 __global__ void k_item_count(const int32_t *__restrict__ par_leaf, const int32_t *__restrict__ leaf_beg, int64_t npar,
                              int chunk, int32_t *__restrict__ cnt) {
@@ -925,6 +1200,62 @@ void leaf_to_leaf(const LeafArgs &a, const Dom &D, cudaStream_t st) {
       else launch_l<32>(la, D, blocks, st);
       JZ_LAUNCH_CHECK();
     }
+  }
+  JZ_CUDA(cudaFreeAsync(cnt, st));
+  JZ_CUDA(cudaFreeAsync(off, st));
+  JZ_CUDA(cudaFreeAsync(item_par, st));
+  JZ_CUDA(cudaFreeAsync(item_q0, st));
+  JZ_CUDA(cudaFreeAsync(leaf_ce, st));
+  if (par_ce) JZ_CUDA(cudaFreeAsync(par_ce, st));
+}
+
+void fof_leaf(const LeafArgs &a, const Dom &D, float b2, int32_t *par, cudaStream_t st) {
+  if (a.npar == 0) return;
+  int32_t *cnt = nullptr;
+  int64_t *off = nullptr;
+  JZ_CUDA(cudaMallocAsync(&cnt, a.npar * sizeof(int32_t), st));
+  JZ_CUDA(cudaMallocAsync(&off, (a.npar + 1) * sizeof(int64_t), st));
+  k_item_count<<<grid_for(a.npar, 256), 256, 0, st>>>(a.par_leaf, a.sbeg, a.npar, 32, cnt);
+  JZ_LAUNCH_CHECK();
+  exclusive_scan_i32_to_i64(cnt, off, a.npar, st);
+  const int64_t nitems = read_i64(off + a.npar, st);
+  int32_t *item_par = nullptr, *item_q0 = nullptr;
+  JZ_CUDA(cudaMallocAsync(&item_par, (nitems + 1) * sizeof(int32_t), st));
+  JZ_CUDA(cudaMallocAsync(&item_q0, (nitems + 1) * sizeof(int32_t), st));
+  k_item_fill<<<grid_for(a.npar, 256), 256, 0, st>>>(a.par_leaf, a.sbeg, a.npar, 32, off, item_par, item_q0);
+  JZ_LAUNCH_CHECK();
+  const float Lmax = D.periodic ? fmaxf(fmaxf(D.L[0], D.L[1]), D.L[2]) : 0.f;
+  CE *leaf_ce = nullptr, *par_ce = nullptr;
+  JZ_CUDA(cudaMallocAsync(&leaf_ce, (a.nleaf > 0 ? a.nleaf : 1) * sizeof(CE), st));
+  k_box_ce<<<grid_for(a.nleaf, 256), 256, 0, st>>>(a.leaf_box, a.nleaf, Lmax, leaf_ce);
+  JZ_LAUNCH_CHECK();
+  if (a.par_box) {
+    JZ_CUDA(cudaMallocAsync(&par_ce, a.npar * sizeof(CE), st));
+    k_box_ce<<<grid_for(a.npar, 256), 256, 0, st>>>(a.par_box, a.npar, Lmax, par_ce);
+    JZ_LAUNCH_CHECK();
+  }
+  FofPK f;
+  f.spts = a.spts;
+  f.sbeg = a.sbeg;
+  f.leaf_ce = leaf_ce;
+  f.par_leaf = a.par_leaf;
+  f.par_ce = par_ce;
+  f.ispl = a.il->ispl;
+  f.isrc = a.il->isrc;
+  f.rlow = a.il->rlow;
+  f.item_par = item_par;
+  f.item_q0 = item_q0;
+  f.nitems = nitems;
+  f.b2 = b2;
+  f.Lmax = Lmax;
+  f.sorted = !(a.flags & (JZ_FLAG_NO_SEGSORT | JZ_FLAG_NO_EARLY_EXIT));
+  f.par = par;
+  f.stats = a.evals;
+  if (nitems > 0) {
+    const unsigned blocks = (unsigned)ceil_div(nitems, kLWarps);
+    if (D.periodic) k_fof_leaf<true><<<blocks, kLThreads, 0, st>>>(f, D);
+    else k_fof_leaf<false><<<blocks, kLThreads, 0, st>>>(f, D);
+    JZ_LAUNCH_CHECK();
   }
   JZ_CUDA(cudaFreeAsync(cnt, st));
   JZ_CUDA(cudaFreeAsync(off, st));

@@ -249,8 +249,12 @@ __global__ void __launch_bounds__(kSegWarps * 32) k_segsort(const int64_t *__res
   }
 }
 
+__global__ void k_fill_f32(float *__restrict__ a, int64_t m, float v) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += (int64_t)gridDim.x * blockDim.x) a[j] = v;
+}
+
 void walk_to(const std::vector<Plane> &planes, const Dom &D, int k, int ngr, unsigned flags, int stop, IList &out_il,
-             float **rmax2_out, int32_t **superbeg_out, cudaStream_t st) {
+             float **rmax2_out, int32_t **superbeg_out, cudaStream_t st, float fixed_r2) {
   const int P = (int)planes.size();
   const int top = P - 1;
   const int64_t ntop = planes[top].nnodes;
@@ -280,8 +284,13 @@ void walk_to(const std::vector<Plane> &planes, const Dom &D, int k, int ngr, uns
     JZ_CUDA(cudaMallocAsync(&cnt, pl.nnodes * sizeof(int32_t), st));
     const int srt = do_sort ? 1 : 0;
     const int ee = early ? 1 : 0;
-    k_n2n<RMAX><<<(unsigned)ceil_div(npar, kN2NWarps), kN2NWarps * 32, 0, st>>>(pbeg, npar, il.ispl, il.isrc, il.rlow, pl.box, D, k, srt, ee,
-                                                        rmax2, nullptr, nullptr, nullptr, nullptr);
+    if (fixed_r2 >= 0.f) {  // fixed-radius walk (friends-of-friends): every node keeps r^2
+      k_fill_f32<<<grid_for(pl.nnodes, 256), 256, 0, st>>>(rmax2, pl.nnodes, fixed_r2);
+    } else {
+      k_n2n<RMAX><<<(unsigned)ceil_div(npar, kN2NWarps), kN2NWarps * 32, 0, st>>>(pbeg, npar, il.ispl, il.isrc, il.rlow,
+                                                                                pl.box, D, k, srt, ee, rmax2, nullptr,
+                                                                                nullptr, nullptr, nullptr);
+    }
     JZ_LAUNCH_CHECK();
     k_n2n<COUNT><<<(unsigned)ceil_div(npar, kN2NWarps), kN2NWarps * 32, 0, st>>>(pbeg, npar, il.ispl, il.isrc, il.rlow, pl.box, D, k, srt, ee,
                                                          rmax2, cnt, nullptr, nullptr, nullptr);

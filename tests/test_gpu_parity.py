@@ -431,3 +431,72 @@ def test_separate_queries_full_size_sampled():
     d = d2.double()
     assert bool((d[:, 1:] >= d[:, :-1]).all()) and bool(torch.isfinite(d).all())
     assert int(idx.min()) >= 0 and int(idx.max()) < 10**7
+
+
+# ----------------------------------------------------------------------------------- F4 friends-of-friends
+def _fof_cmp(pos, r, box, min_count=20):
+    from oracle import fof_catalogue, fof_labels
+
+    jz = _jz()
+    lab, cat = jz.fof(torch.from_numpy(np.ascontiguousarray(pos)).cuda(), r, box=box, min_count=min_count)
+    lab = lab.cpu().numpy()
+    want = fof_labels(pos, r, box)
+    assert np.array_equal(lab, want), f"{(lab != want).sum()} labels differ"
+    u, c, com, rad = fof_catalogue(pos, want, box, min_count)
+    order = np.argsort(cat["label"].cpu().numpy(), kind="stable")
+    assert np.array_equal(cat["label"].cpu().numpy()[order], u)
+    assert np.array_equal(cat["count"].cpu().numpy()[order], c)
+    got_com = cat["com"].cpu().numpy()[order]
+    if box is not None:  # compare on the circle: a centre at ~0 may come back as ~L
+        dd = got_com - com
+        L = np.broadcast_to(np.asarray(box, np.float64), (3,))
+        dd -= L * np.round(dd / L)
+        assert np.abs(dd).max(initial=0) <= 1e-9
+    else:
+        assert np.allclose(got_com, com, rtol=1e-9, atol=1e-12)
+    assert np.allclose(cat["rad"].cpu().numpy()[order], rad, rtol=1e-7, atol=1e-12)
+    return len(np.unique(want))
+
+
+@pytest.mark.parametrize("kind,box", [("uniform", 1.0), ("uniform", None), ("clustered", 1.0), ("clustered", None),
+                                      ("dups", 1.0), ("lattice", 1.0), ("normal", None)])
+def test_fof_labels_and_catalogue(kind, box):
+    """F4 (P:L466-504): labels bit-identical to the oracle's components, catalogue (count exact;
+    centre of mass / inertia radius FP64 within 1e-9 / 1e-7 relative: atomics sum in any order)."""
+    from synth import normal_points
+
+    if kind == "uniform":
+        pos, r = uniform_points(60000, 51, 1.0), 0.2 * 60000 ** (-1 / 3) * 3
+    elif kind == "clustered":
+        pos, r = clustered_points(80000, 52, 1.0), 0.2 * 80000 ** (-1 / 3)
+    elif kind == "dups":
+        q = uniform_points(3000, 53, 1.0)
+        pos, r = np.concatenate([q, q, q[:500], np.repeat(q[:2], 300, axis=0)]), 0.02
+    elif kind == "lattice":
+        pos, r = lattice_points(16, 1.0 / 16), 1.0 / 16  # every lattice neighbour exactly at r: one group
+    else:
+        pos, r = normal_points(50000, 54), 0.05
+    ng = _fof_cmp(pos, r, box, min_count=2)
+    assert ng >= 1
+
+
+def test_fof_extremes_and_errors():
+    """r = 0 links only exact duplicates; a huge r links everything; FoF on a separate-query index
+    is refused."""
+    jz = _jz()
+    q = uniform_points(2000, 55, 1.0)
+    pos = np.concatenate([q, q[:100]])
+    _fof_cmp(pos, 0.0, 1.0, min_count=2)
+    lab, cat = jz.fof(torch.from_numpy(pos).cuda(), 2.0, box=None, min_count=1)
+    assert (lab.cpu().numpy() == 0).all() and cat["count"].cpu().tolist() == [len(pos)]
+    ix = jz.KnnIndex(torch.from_numpy(q).cuda(), box=1.0, queries=torch.from_numpy(q[:10]).cuda())
+    with pytest.raises(Exception):
+        ix.fof(0.01)
+    ix.free()
+
+
+def test_fof_c4_distribution_full():
+    """F4 on 10^6 points of the C4 (clustered) distribution, b = 0.2 mean separations, every
+    label vs the grid oracle."""
+    pos, box, _ = make_config("C4", n=1_000_000)
+    _fof_cmp(pos, 0.2 * 1e6 ** (-1 / 3), box, min_count=20)
