@@ -48,6 +48,9 @@ static_assert(JZ_LCAP >= kMaxLeaf, "a leaf must fit the staging buffer");
 #ifndef JZ_HALFGATE
 #define JZ_HALFGATE 1
 #endif
+#ifndef JZ_STATS
+#define JZ_STATS 1  // per-lane walk counters (appends, merge rounds, compactions, staged leaves)
+#endif
 #ifndef JZ_MERGE_MIN
 #define JZ_MERGE_MIN 1
 #endif
@@ -223,7 +226,7 @@ template <int K, bool LB>
 __device__ __forceinline__ void merge(WarpBuf<K> &B, Lane<K, LB> &L) {
   const int lane = threadIdx.x & 31;
   const int nr = (int)__reduce_max_sync(0xffffffffu, (unsigned)(L.nl - L.nf));
-  L.rnd += nr;
+  if (JZ_STATS) L.rnd += nr;
   unsigned nx = L.nf < L.nl ? B.ld[L.nf][lane] : 0x7f800000u;
 #pragma unroll 1
   for (int i = 0; i < nr; ++i) {
@@ -232,7 +235,7 @@ __device__ __forceinline__ void merge(WarpBuf<K> &B, Lane<K, LB> &L) {
     nx = r + 1 < L.nl ? B.ld[r + 1][lane] : 0x7f800000u;  // prefetch the next round's entry
     const bool in = d < L.F[K - 1];
     if (__any_sync(0xffffffffu, in)) bubble<K>(L.F, d);
-    L.ins += in;
+    if (JZ_STATS) L.ins += in;
   }
   L.nf = L.nl;
   L.kth = L.act ? L.F[K - 1] : -1.f;
@@ -264,7 +267,7 @@ template <int K, bool LB>
 __device__ __forceinline__ void compact(WarpBuf<K> &B, Lane<K, LB> &L) {
   constexpr int C = LogCap<K>::C;
   const int lane = threadIdx.x & 31;
-  ++L.cmp;
+  if (JZ_STATS) ++L.cmp;
   merge<K, LB>(B, L);
   const unsigned kb = __float_as_uint(L.kth);
   const int r1 = (int)__reduce_max_sync(0xffffffffu, (unsigned)L.nl);
@@ -302,7 +305,7 @@ __device__ __forceinline__ void append(WarpBuf<K> &B, Lane<K, LB> &L, float d2, 
       B.ld[L.nl][threadIdx.x & 31] = __float_as_uint(d2);
       B.lg[L.nl][threadIdx.x & 31] = (unsigned)(g + 1);
       ++L.nl;
-      ++L.app;
+      if (JZ_STATS) ++L.app;
     }
   }
 }
