@@ -26,6 +26,8 @@
 //    the k smallest keys of the log are the row (bitonic sort in registers). The list starts
 //    full of R_max^2(J), which bounds every contained query's k-th distance.
 //  * Rows are written straight to their final place (input or z order): no reorder pass.
+#include <cstdio>
+
 #include "jz_common.cuh"
 #include "jz_internal.h"
 
@@ -198,6 +200,14 @@ __device__ __forceinline__ void bubble(float (&F)[K], float d) {
   }
 }
 
+#ifdef JZ_DIAG_WALK
+__device__ unsigned long long g_diag[8];  // [0] entries reached [1] entries passing the node test [2] 32-leaf chunks
+                                           // [3] leaves passing the warp test [4] leaves staged [5] items
+#define JZ_DIAG(i, v) (((threadIdx.x & 31) == 0) ? (void)atomicAdd(&g_diag[i], (unsigned long long)(v)) : (void)0)
+#else
+#define JZ_DIAG(i, v) ((void)0)
+#endif
+
 template <int K>
 struct WarpBuf {
   float x[kLCap + 8], y[kLCap + 8], z[kLCap + 8];  // + 8: padding to a multiple of 8
@@ -220,6 +230,23 @@ struct Lane {
   unsigned stg;   // staged leaves (warp-uniform)
   bool act;
 };
+
+// sort a bitonic sequence ascending (half-cleaner stages)
+template <int K>
+__device__ __forceinline__ void bitonic_merge_f(float (&T)[K]) {
+#pragma unroll
+  for (int stride = K >> 1; stride > 0; stride >>= 1) {
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      const int j = i ^ stride;
+      if (j > i) {
+        const float lo = fminf(T[i], T[j]), hi = fmaxf(T[i], T[j]);
+        T[i] = lo;
+        T[j] = hi;
+      }
+    }
+  }
+}
 
 // merge the lane's new log entries into F (all lanes in lockstep: max(new) rounds)
 template <int K, bool LB>
@@ -493,6 +520,8 @@ __device__ __forceinline__ void visit_leaves(const LeafPK &a, const Dom &D, Warp
       }
     }
     unsigned bal = __ballot_sync(0xffffffffu, pass);
+    JZ_DIAG(2, 1);
+    JZ_DIAG(3, __popc(bal));
     while (bal) {
       // batch consecutive surviving leaves of one shift class into the warp buffer
       const int c0 = __shfl_sync(0xffffffffu, cls, __ffs(bal) - 1);
@@ -525,6 +554,7 @@ __device__ __forceinline__ void visit_leaves(const LeafPK &a, const Dom &D, Warp
           B.g[n + t] = __float_as_int(p.w);
         }
         nev += act ? (unsigned)m : 0u;
+        JZ_DIAG(4, 1);
 #ifndef JZ_DIAG_OWN
         ++L.stg;
 #endif
@@ -597,23 +627,6 @@ template <int K>
 struct WinN {
   static constexpr int N = (JZ_WIN2 && K <= 16) ? 2 * K : K;
 };
-
-// sort a bitonic sequence ascending (half-cleaner stages)
-template <int K>
-__device__ __forceinline__ void bitonic_merge_f(float (&T)[K]) {
-#pragma unroll
-  for (int stride = K >> 1; stride > 0; stride >>= 1) {
-#pragma unroll
-    for (int i = 0; i < K; ++i) {
-      const int j = i ^ stride;
-      if (j > i) {
-        const float lo = fminf(T[i], T[j]), hi = fmaxf(T[i], T[j]);
-        T[i] = lo;
-        T[j] = hi;
-      }
-    }
-  }
-}
 
 // z-window initialisation (self-query): the N = WinN<K>::N sources at sorted positions
 // [wpos, wpos + N) around the lane's own query are evaluated first; their keys start the log
@@ -775,22 +788,39 @@ __global__ void __launch_bounds__(kLThreads, JZ_MINB) k_leaf(LeafPK a, Dom D) {
 #endif
   }
   const int64_t eb = a.ispl[J], ee = a.ispl[J + 1];
-  for (int64_t e = eb; e < ee; ++e) {
-    const int S = a.isrc[e];
-    const float wmax = a.early ? warp_max_kth(L.kth) : INFINITY;
-    if (a.rlow[e] > wmax) {
-      if (a.sorted) break;
-      continue;
+  // entries in chunks of 32, one lane per entry (list order = r_low order): the node tests run in
+  // parallel instead of one dependent load chain per entry; survivors are visited in list order
+  for (int64_t c0 = eb; c0 < ee; c0 += 32) {
+    const float wc = a.early ? warp_max_kth(L.kth) : INFINITY;
+    const int64_t e = c0 + lane;
+    bool ok = false, past = false;
+    int S = 0;
+    if (e < ee) {
+      const float rl = a.rlow[e];
+      S = a.isrc[e];
+      past = rl > wc;
+      ok = !past;
+      if (ok && a.par_ce) {
+        const CE pc = a.par_ce[S];
+        ok = dlow2_ce<PER>(__fsub_rn(wb.c.x, pc.c.x), __fsub_rn(wb.c.y, pc.c.y), __fsub_rn(wb.c.z, pc.c.z),
+                           __fadd_ru(wb.e.x, pc.e.x), __fadd_ru(wb.e.y, pc.e.y), __fadd_ru(wb.e.z, pc.e.z), D) <= wc;
+      }
     }
-    if (a.par_ce) {
-      const CE pc = a.par_ce[S];
-      const float d = dlow2_ce<PER>(__fsub_rn(wb.c.x, pc.c.x), __fsub_rn(wb.c.y, pc.c.y), __fsub_rn(wb.c.z, pc.c.z),
-                                    __fadd_ru(wb.e.x, pc.e.x), __fadd_ru(wb.e.y, pc.e.y), __fadd_ru(wb.e.z, pc.e.z), D);
-      if (d > wmax) continue;
+    JZ_DIAG(0, __popc(__ballot_sync(0xffffffffu, e < ee && !past)));
+    unsigned bal = __ballot_sync(0xffffffffu, ok);
+    JZ_DIAG(1, __popc(bal));
+    const bool stop = a.sorted && __any_sync(0xffffffffu, past);  // later chunks have larger r_low
+    while (bal) {
+      const int src = __ffs(bal) - 1;
+      bal &= bal - 1;
+      const int Se = __shfl_sync(0xffffffffu, S, src);
+      const float wmax = a.early ? warp_max_kth(L.kth) : INFINITY;
+      visit_leaves<K, LB, PER>(a, D, B, wb, wmax, a.par_leaf[Se], a.par_leaf[Se + 1], Se == J ? xa : 0,
+                               Se == J ? xb : 0, qx, qy, qz, act, L, nev);
     }
-    visit_leaves<K, LB, PER>(a, D, B, wb, wmax, a.par_leaf[S], a.par_leaf[S + 1], S == J ? xa : 0, S == J ? xb : 0, qx,
-                             qy, qz, act, L, nev);
+    if (stop) break;
   }
+  JZ_DIAG(5, 1);
   // the row: the k smallest keys of the log (all entries <= the final k-th value)
   compact<K, LB>(B, L);
   if (L.nl > a.k) L.nl = drop_largest<K>(B, L.nl, a.k);
@@ -1208,6 +1238,18 @@ void leaf_to_leaf(const LeafArgs &a, const Dom &D, cudaStream_t st) {
   JZ_CUDA(cudaFreeAsync(off, st));
   JZ_CUDA(cudaFreeAsync(item_par, st));
   JZ_CUDA(cudaFreeAsync(item_q0, st));
+#ifdef JZ_DIAG_WALK
+  {
+    unsigned long long h[8];
+    JZ_CUDA(cudaMemcpyFromSymbolAsync(h, g_diag, sizeof(h), 0, cudaMemcpyDeviceToHost, st));
+    JZ_CUDA(cudaStreamSynchronize(st));
+    const double it = h[5] ? (double)h[5] : 1.0;
+    fprintf(stderr, "JZ_DIAG per item: entries %.1f passing %.1f chunks %.1f leaves_warp %.1f staged %.1f (items %llu)\n",
+            h[0] / it, h[1] / it, h[2] / it, h[3] / it, h[4] / it, h[5]);
+    const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    JZ_CUDA(cudaMemcpyToSymbolAsync(g_diag, z, sizeof(z), 0, cudaMemcpyHostToDevice, st));
+  }
+#endif
   JZ_CUDA(cudaFreeAsync(leaf_ce, st));
   if (par_ce) JZ_CUDA(cudaFreeAsync(par_ce, st));
 }
