@@ -60,9 +60,19 @@ static_assert(JZ_LCAP >= kMaxLeaf, "a leaf must fit the staging buffer");
 #define JZ_MERGE_EACH 0
 #endif
 
+#ifndef JZ_LOGX32
+#define JZ_LOGX32 16  // K = 32: 48-entry log (14 KB per warp with staging) -> 7 CTAs per SM
+#endif
+#ifndef JZ_MINB32
+#define JZ_MINB32 7  // K = 32: 144 registers, no spills (the K = 16 budget of 96 spilled: C3 48 -> 33 ms)
+#endif
 template <int K>
 struct LogCap {
-  static constexpr int C = K + JZ_LOGX;  // log entries per lane
+  static constexpr int C = K + (K > 16 ? JZ_LOGX32 : JZ_LOGX);  // log entries per lane
+};
+template <int K>
+struct MinBlocks {
+  static constexpr int v = K > 16 ? JZ_MINB32 : JZ_MINB;  // CTAs per SM the register budget targets
 };
 
 typedef unsigned long long u64;
@@ -698,7 +708,7 @@ __device__ __forceinline__ void own_pass(const LeafPK &a, const Dom &D, WarpBuf<
 }
 
 template <int K, bool LB, bool PER>
-__global__ void __launch_bounds__(kLThreads, JZ_MINB) k_leaf(LeafPK a, Dom D) {
+__global__ void __launch_bounds__(kLThreads, MinBlocks<K>::v) k_leaf(LeafPK a, Dom D) {
   __shared__ __align__(16) WarpBuf<K> s_buf[kLWarps];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t item = (int64_t)blockIdx.x * kLWarps + warp;
