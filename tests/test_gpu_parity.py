@@ -316,6 +316,30 @@ def test_c4_full_size_sampled():
     assert bool((d2[:, 0] == 0).all())
 
 
+def test_c5_full_size_sampled():
+    """C5 at its full size on one B200 (2^30 uniform points, periodic, k = 8; BASELINE.json config 5
+    is the 8-GPU run, one GPU holds it: ~60 GB of index + 8.6 GB of rows): sampled rows vs the grid
+    oracle over all 2^30 points, plus the row invariants on every row (on device)."""
+    jz = _jz()
+    pos, box, k = make_config("C5")
+    t = torch.from_numpy(pos).cuda()
+    ix = jz.KnnIndex(t, box=box)
+    idx, d2 = ix.query(k)
+    ix.free()
+    del t
+    rows = np.random.default_rng(5).choice(len(pos), 1000, replace=False)
+    sel = torch.from_numpy(rows).cuda()
+    gi, gd = idx[sel].cpu().numpy(), d2[sel].cpu().numpy()
+    assert bool((idx >= 0).all()) and bool((idx < len(pos)).all())
+    assert bool((d2[:, 1:] >= d2[:, :-1]).all())
+    tie = d2[:, 1:] == d2[:, :-1]
+    assert bool((idx[:, 1:][tie] > idx[:, :-1][tie]).all())
+    assert bool((d2[:, 0] == 0).all())
+    del idx, d2, tie
+    io, do = knn_grid(pos, k, box, rows=rows)
+    _assert_same(gi, gd, io, do)
+
+
 # ----------------------------------------------------------------------------------- F1
 # SURVEY.md §8(f) F1: separate query points (joint tree over both types, PAPER.md L272-279)
 # and k > k_max = 32 (ceil(k/32) LeafToLeaf passes with the (d2, index) lower bound, L386).
