@@ -94,6 +94,42 @@ __global__ void k_scatter_rows(const int32_t *__restrict__ rows, int64_t m, int 
   }
 }
 
+// Cheap per-leaf bound on every contained query's local k-th distance (no walk): the smallest
+// ancestor-or-self node holding >= k (source) points contains k candidates within its own AABB, so
+// its self d_up^2 (the AABB diagonal, an exact upper bound on any canonical d2 inside, R8) bounds
+// the k-th distance; +inf if no node holds k points. planes: beg/leafspl/box of every plane.
+struct PlaneRef {
+  const int32_t *leafspl;
+  const NodeBox *box;
+  int64_t nnodes;
+};
+__global__ void k_leaf_rdiag(const NodeBox *__restrict__ leafbox, int64_t nleaf, const PlaneRef *__restrict__ up,
+                             int nup, Dom D, int k, float *__restrict__ r2) {
+  for (int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; l < nleaf; l += (int64_t)gridDim.x * blockDim.x) {
+    NodeBox b = leafbox[l];
+    float r = INFINITY;
+    if (box_count(b) >= k) {
+      r = box_dup2(b, b, D);
+    } else {
+      for (int p = 0; p < nup; ++p) {  // ancestor on plane p+1: node i with leafspl[i] <= l < leafspl[i+1]
+        const PlaneRef pr = up[p];
+        int64_t lo = 0, hi = pr.nnodes - 1;
+        while (lo < hi) {
+          const int64_t mid = (lo + hi + 1) >> 1;
+          if (pr.leafspl[mid] <= l) lo = mid;
+          else hi = mid - 1;
+        }
+        b = pr.box[lo];
+        if (box_count(b) >= k) {
+          r = box_dup2(b, b, D);
+          break;
+        }
+      }
+    }
+    r2[l] = r;
+  }
+}
+
 // leaf R_max^2 -> plane-level boxes with max r2
 __global__ void k_plane_qboxes(const NodeBox *__restrict__ box, const int32_t *__restrict__ leafspl, int64_t nnodes,
                                const float *__restrict__ rmax2_leaf, int rank, float *__restrict__ out) {
@@ -349,10 +385,21 @@ int jz_knn_query_boxes(jz_knn_index *ix, int k, int plane, int rank, float *boxe
       std::vector<float> inf(pl[0].nnodes, INFINITY);
       JZ_CUDA(cudaMemcpyAsync(rmax2, inf.data(), inf.size() * sizeof(float), cudaMemcpyHostToDevice, st));
       JZ_CUDA(cudaStreamSynchronize(st));
-    } else {
+    } else if (v.flags & JZ_FLAG_QBOX_WALK) {  // R_max from the NodeToNode walk to the leaf plane (tighter, slower)
       int32_t *sb = nullptr;
       jz::walk_to(pl, v.D, k, v.ngr, v.flags, 0, il, &rmax2, &sb, st);
       il.release(st);
+    } else {  // default: the diagonal of the smallest ancestor holding k points (no walk)
+      const int nup = (int)pl.size() - 1;
+      std::vector<jz::PlaneRef> h(nup > 0 ? nup : 1);
+      for (int p = 1; p < (int)pl.size(); ++p) h[p - 1] = jz::PlaneRef{pl[p].leafspl, pl[p].box, pl[p].nnodes};
+      jz::PlaneRef *dup = nullptr;
+      JZ_CUDA(cudaMallocAsync(&dup, h.size() * sizeof(jz::PlaneRef), st));
+      JZ_CUDA(cudaMemcpyAsync(dup, h.data(), h.size() * sizeof(jz::PlaneRef), cudaMemcpyHostToDevice, st));
+      JZ_CUDA(cudaMallocAsync(&rmax2, pl[0].nnodes * sizeof(float), st));
+      jz::k_leaf_rdiag<<<jz::grid_for(pl[0].nnodes, 256), 256, 0, st>>>(pl[0].box, pl[0].nnodes, dup, nup, v.D, k, rmax2);
+      JZ_LAUNCH_CHECK();
+      JZ_CUDA(cudaFreeAsync(dup, st));
     }
     jz::k_plane_qboxes<<<jz::grid_for(pl[plane].nnodes, 128), 128, 0, st>>>(pl[plane].box, pl[plane].leafspl,
                                                                              pl[plane].nnodes, rmax2, rank, boxes);
