@@ -258,6 +258,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true", help="kernel-only run for ncu (no e2e / baseline / clocks)")
+    ap.add_argument("--dist", action="store_true", help="use the multi-GPU path even with one rank (tests)")
     ap.add_argument("--order", default=None, choices=["z", "input"],
                     help="row order under torchrun (default z: rows + global ids, P:L458; input: F2 reverse exchange)")
     args = ap.parse_args()
@@ -265,7 +266,7 @@ def main():
         run_reference(args)
         return
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    if world > 1:
+    if world > 1 or args.dist:
         from paper_2604_05885_b200.dist import run_bench_distributed
 
         run_bench_distributed(args, METRIC, UNIT)

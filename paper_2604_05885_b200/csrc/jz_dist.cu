@@ -5,8 +5,9 @@
 //   jz_morton_keys          keys in one global frame (every rank gets identical keys)
 //   jz_bucket_by_splitters  dest rank = #splitters <= key (Morton-range partition)
 //   jz_pack_by_rank         float4 {x, y, z, bits(gidx)} grouped by destination rank
-//   jz_knn_query_boxes      per node of a plane: AABB + max R_max^2 of its leaves, from the
-//                           NodeToNode walk down to the leaf plane (Alg. 1 lines 1-5)
+//   jz_knn_query_boxes      per node of a plane: AABB + max R_max^2 of its leaves (default: the
+//                           AABB diagonal of the smallest ancestor holding k points; with
+//                           JZ_FLAG_QBOX_WALK the NodeToNode walk to the leaf plane, Alg. 1 l. 1-5)
 //   jz_knn_select_ghosts    bitmask of peer ranks whose query boxes a local leaf reaches
 //                           (exact monotone box bound d_low^2 <= r2; leaf granularity is a
 //                           superset of the required points, so no neighbour can be missed)
@@ -44,12 +45,24 @@ __global__ void k_bucket(const uint64_t *__restrict__ keys, int64_t n, const uin
     if (s_c[i]) atomicAdd(&counts[i], s_c[i]);
 }
 
+// Slot for this lane in destination r's group: one atomic per (warp, destination) instead of one
+// per point (1e8 same-address atomics cost 65 ms at R = 1); order inside a group unspecified.
+__device__ __forceinline__ unsigned long long warp_slot(unsigned long long *cursor, int r) {
+  const unsigned act = __activemask();
+  const unsigned peers = __match_any_sync(act, r);
+  const int lane = threadIdx.x & 31, leader = __ffs(peers) - 1;
+  unsigned long long base = 0;
+  if (lane == leader) base = atomicAdd(&cursor[r], (unsigned long long)__popc(peers));
+  base = __shfl_sync(peers, base, leader);
+  return base + (unsigned long long)__popc(peers & ((1u << lane) - 1u));
+}
+
 __global__ void k_pack(const float *__restrict__ pos, int64_t n, int64_t gbase, const int32_t *__restrict__ dest,
                        const int64_t *__restrict__ off, unsigned long long *__restrict__ cursor,
                        float4 *__restrict__ out) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int r = dest[i];
-    const unsigned long long p = atomicAdd(&cursor[r], 1ull);
+    const unsigned long long p = warp_slot(cursor, r);
     out[off[r] + (int64_t)p] = make_float4(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2], __int_as_float((int)(gbase + i)));
   }
 }
@@ -59,7 +72,7 @@ __global__ void k_row_slots(const int32_t *__restrict__ dest, int64_t m, const i
                             unsigned long long *__restrict__ cursor, int64_t *__restrict__ slot) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
     const int r = dest[i];
-    slot[i] = off[r] + (int64_t)atomicAdd(&cursor[r], 1ull);
+    slot[i] = off[r] + (int64_t)warp_slot(cursor, r);
   }
 }
 
@@ -235,13 +248,12 @@ __global__ void k_ghost_pack(const float4 *__restrict__ pts, const int32_t *__re
                              const int64_t *__restrict__ off, unsigned long long *__restrict__ cursor,
                              float4 *__restrict__ out) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    int m = mask[i];
-    while (m) {
-      int r = __ffs(m) - 1;
-      m &= m - 1;
-      if (r >= nranks) continue;
-      const unsigned long long p = atomicAdd(&cursor[r], 1ull);
-      out[off[r] + (int64_t)p] = pts[i];
+    const int m = mask[i];
+    for (int r = 0; r < nranks; ++r) {  // rank-uniform loop: lanes flagged for r share one atomic
+      if ((m >> r) & 1) {
+        const unsigned long long p = warp_slot(cursor, r);
+        out[off[r] + (int64_t)p] = pts[i];
+      }
     }
   }
 }

@@ -166,9 +166,10 @@ class SimComm(Comm):
 class GpuBackend:
     """Per-rank compute through the C ABI (all steps are library kernels)."""
 
-    def __init__(self, params=None, stream=None):
+    def __init__(self, params=None, stream=None, stats=None):
         from . import _binding as B
 
+        self.stats = stats
         self.B = B
         self.lib = B.lib()
         self.params = params
@@ -265,7 +266,12 @@ class GpuBackend:
         return out[: sum(counts)]
 
     def query_z(self, ix, k):
-        return ix.query(k, order="z")
+        out = ix.query(k, order="z")
+        if self.stats is not None:  # LeafToLeaf time / evaluations of the final walk (bench roofline)
+            t = ix.stage_times()
+            self.stats["leaf2leaf_ms"] = t["leaf2leaf"]
+            self.stats["evals"] = t["evals"]
+        return out
 
     def pack_rows(self, idx, d2, rowg, dest, counts):
         k = idx.shape[1]
@@ -325,6 +331,9 @@ def dist_knn(pos: torch.Tensor, gidx_base: int, k: int, box, comm: Comm, backend
         ext = float(max(np.float32(hi_np[d] - lo_np[d]) for d in range(3)))
         frame = {"box": None, "origin": [float(x) for x in lo_np], "extent": ext if ext > 0 else 1.0}
     keys = backend.morton_keys(pos, frame)
+    if timings is not None:
+        torch.cuda.synchronize()
+        t["keys"] = time.perf_counter() - t0
     # 2. splitters
     samp = backend.sample(keys, n_samp, seed * 1000003 + r)
     allsamp = torch.cat(comm.all_gather_v(samp))
@@ -445,9 +454,12 @@ def run_ranks_simulated(pos_np: np.ndarray, k: int, box, R: int, params=None, n_
 
 # ----------------------------------------------------------------------------- bench (torchrun)
 def run_bench_distributed(args, metric, unit):
-    """bench.py under torchrun: C4 (10^8 clustered, k = 16) split across ranks (strong scaling)."""
+    """bench.py under torchrun: C4 (10^8 clustered, k = 16) split across ranks (strong scaling).
+    Device time per step = max over ranks (CUDA events on each rank's stream); e2e = the same
+    with each rank's slice copied from pinned host memory and its rows copied back every step."""
     import json
     import os
+    import sys
 
     import torch.distributed as dist
 
@@ -464,36 +476,93 @@ def run_bench_distributed(args, metric, unit):
     pos, box, k = make_config(args.config, n=n, start=lo, stop=hi)
     d_pos = torch.from_numpy(pos).cuda()
     comm = TorchComm()
-    be = GpuBackend()
+    stats = {}
+    be = GpuBackend(stats=stats)
     from . import _binding as B
+    from . import set_timing
 
+    set_timing(True)
     order = getattr(args, "order", None) or "z"
 
+    tdict = {}
+
     def step():
-        return dist_knn(d_pos, lo, k, box, comm, be, order=order)
+        return dist_knn(d_pos, lo, k, box, comm, be, order=order, timings=tdict)
 
     for _ in range(args.warmup):
         step()
+    if os.environ.get("JZ_DIST_TIMES") == "1":
+        torch.cuda.synchronize()
+        print(f"rank {rank} phase wall times (last warm-up step): "
+              + ", ".join(f"{kk} {vv * 1e3:.1f} ms" if isinstance(vv, float) else f"{kk} {vv}" for kk, vv in tdict.items()),
+              file=sys.stderr, flush=True)
     torch.cuda.synchronize()
     comm.barrier()
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    clk = None
+    if not getattr(args, "profile", False):
+        from bench import ClockSampler
+
+        clk = ClockSampler(local_rank)
+        clk.start()
     l0 = B.lib().jz_launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    comm.barrier()
     e0.record()
     for _ in range(args.steps):
         step()
     e1.record()
     torch.cuda.synchronize()
+    comm.barrier()
+    clocks = clk.stop() if clk is not None else None
     ms = e0.elapsed_time(e1) / args.steps
     ms_max = comm.max_scalar(ms)
     launches = B.lib().jz_launch_count() - l0
+    l2l = comm.max_scalar(stats.get("leaf2leaf_ms", 0.0))
+    evals = float(stats.get("evals", 0))
+    # e2e: pinned host slice -> device -> distributed kNN -> rows back to pinned host memory
+    e2e = None
+    if not getattr(args, "no_e2e", False) and not getattr(args, "profile", False):
+        h_pos = torch.from_numpy(pos).pin_memory()
+        steps = max(1, min(args.steps, 3))
+        res = dist_knn(h_pos.to("cuda", non_blocking=True), lo, k, box, comm, be, order=order)  # untimed: pin outputs
+        outs = [torch.empty(r.shape, dtype=r.dtype).pin_memory() for r in res]
+        del res
+        torch.cuda.synchronize()
+        comm.barrier()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record()
+        h2d = d2h = 0
+        for _ in range(steps):
+            dp = h_pos.to("cuda", non_blocking=True)
+            res = dist_knn(dp, lo, k, box, comm, be, order=order)
+            for o, r in zip(outs, res):
+                o.copy_(r, non_blocking=True)
+            h2d = dp.numel() * 4
+            d2h = sum(r.numel() * r.element_size() for r in res)
+        t1.record()
+        torch.cuda.synchronize()
+        e2e_ms = comm.max_scalar(t0.elapsed_time(t1) / steps)
+        e2e = {"value": n / (e2e_ms / 1e3), "unit": unit, "h2d_bytes_per_step": int(comm.max_scalar(h2d) * world),
+               "d2h_bytes_per_step": int(comm.max_scalar(d2h) * world), "ms_per_step": e2e_ms,
+               "api": "dist_knn (pinned host slice per rank, rows back to pinned host memory)"}
     if rank == 0:
+        peak = 148 * 128 * 1965e6 / 1e12
+        achieved = evals * 6 / (stats.get("leaf2leaf_ms", 0.0) / 1e3) / 1e12 if stats.get("leaf2leaf_ms") else 0.0
         line = {"metric": metric, "value": n / (ms_max / 1e3), "unit": unit, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                 "config": {"workload": args.config, "n_points": n, "k": k, "box": "periodic L=1" if box else "open",
                            "distribution": c["kind"],
                            "order": "z (rows + global ids)" if order == "z" else "input (F2 reverse all-to-all-v)",
-                           "parallelism": f"Morton-range partition x{world} + ghost exchange (NCCL)"},
-                "gpu_launches": int(launches)}
+                           "parallelism": f"Morton-range partition x{world} + ghost exchange (NCCL)",
+                           "l2": "inputs and rows exceed the 126 MB L2; no flush"},
+                "roofline": {"bound": "alu", "kernel": "k_leaf2leaf (LeafToLeaf), rank 0", "achieved": achieved,
+                             "peak": peak, "unit": "T FP32 lane-ops/s", "frac": achieved / peak, "traffic": None,
+                             "work": f"{int(evals)} distance evaluations x 6 FP32 ops on rank 0",
+                             "ms_per_launch": stats.get("leaf2leaf_ms"), "max_over_ranks_ms": l2l},
+                "gpu_launches": int(launches), "clocks": clocks, "e2e": e2e}
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
