@@ -39,7 +39,7 @@ constexpr int kLThreads = kLWarps * 32;
 #define JZ_LCAP 128
 #endif
 #ifndef JZ_MINB
-#define JZ_MINB 9  // 9 CTAs x 2 warps per SM: 112 registers (smem allows 9 CTAs at K = 16)
+#define JZ_MINB 9  // 9 CTAs x 2 warps per SM: 96 registers (5 warps per SM partition; smem allows 9 CTAs at K = 16)
 #endif
 constexpr int kLCap = JZ_LCAP;  // staged source points per warp (2 KB SoA); >= the largest leaf (kMaxLeaf)
 static_assert(JZ_LCAP >= kMaxLeaf, "a leaf must fit the staging buffer");
@@ -47,17 +47,8 @@ static_assert(JZ_LCAP >= kMaxLeaf, "a leaf must fit the staging buffer");
 #ifndef JZ_LOGX
 #define JZ_LOGX 24
 #endif
-#ifndef JZ_HALFGATE
-#define JZ_HALFGATE 1
-#endif
 #ifndef JZ_STATS
 #define JZ_STATS 1  // per-lane walk counters (appends, merge rounds, compactions, staged leaves)
-#endif
-#ifndef JZ_MERGE_MIN
-#define JZ_MERGE_MIN 1
-#endif
-#ifndef JZ_MERGE_EACH
-#define JZ_MERGE_EACH 0
 #endif
 
 #ifndef JZ_LOGX32
@@ -177,36 +168,19 @@ __global__ void k_box_ce(const NodeBox *__restrict__ box, int64_t n, float Lmax,
 // insert value d into the sorted list F, dropping the largest (identity when d >= F[K-1]):
 // F'[j] = max(F[j-1], min(F[j], d)), F'[0] = min(F[0], d) -- every slot independent (depth 2,
 // no serial chain). Warp-converged: the lower half runs only when some lane's d lands there.
-#ifndef JZ_PAR_INSERT
-#define JZ_PAR_INSERT 1
-#endif
+// insert value d into the sorted list F, dropping the largest (identity when d >= F[K-1]):
+// F'[j] = max(F[j-1], min(F[j], d)), F'[0] = min(F[0], d) -- every slot independent (depth 2, no
+// serial chain); the lower half runs only when some lane's d lands there (late insertions land
+// in the upper half). Warp-converged callers only.
 template <int K>
 __device__ __forceinline__ void bubble(float (&F)[K], float d) {
-  constexpr int J0 = JZ_HALFGATE ? K / 2 : 0;
-  if (JZ_PAR_INSERT) {
+  constexpr int J0 = K / 2;
 #pragma unroll
-    for (int j = K - 1; j >= J0 && j > 0; --j) F[j] = fmaxf(F[j - 1], fminf(F[j], d));
-    if (J0 > 0 && __any_sync(0xffffffffu, d < F[J0 > 0 ? J0 - 1 : 0])) {
+  for (int j = K - 1; j >= J0 && j > 0; --j) F[j] = fmaxf(F[j - 1], fminf(F[j], d));
+  if (__any_sync(0xffffffffu, d < F[J0 > 0 ? J0 - 1 : 0])) {
 #pragma unroll
-      for (int j = J0 - 1; j > 0; --j) F[j] = fmaxf(F[j - 1], fminf(F[j], d));
-      F[0] = fminf(F[0], d);
-    }
-    if (J0 == 0) F[0] = fminf(F[0], d);
-  } else {
-    if (J0 > 0 && __any_sync(0xffffffffu, d < F[J0 > 0 ? J0 - 1 : 0])) {
-#pragma unroll
-      for (int j = 0; j < J0; ++j) {
-        const float lo = fminf(F[j], d);
-        d = fmaxf(F[j], d);
-        F[j] = lo;
-      }
-    }
-#pragma unroll
-    for (int j = J0; j < K; ++j) {
-      const float lo = fminf(F[j], d);
-      d = fmaxf(F[j], d);
-      F[j] = lo;
-    }
+    for (int j = J0 - 1; j > 0; --j) F[j] = fmaxf(F[j - 1], fminf(F[j], d));
+    F[0] = fminf(F[0], d);
   }
 }
 
@@ -240,23 +214,6 @@ struct Lane {
   unsigned stg;   // staged leaves (warp-uniform)
   bool act;
 };
-
-// sort a bitonic sequence ascending (half-cleaner stages)
-template <int K>
-__device__ __forceinline__ void bitonic_merge_f(float (&T)[K]) {
-#pragma unroll
-  for (int stride = K >> 1; stride > 0; stride >>= 1) {
-#pragma unroll
-    for (int i = 0; i < K; ++i) {
-      const int j = i ^ stride;
-      if (j > i) {
-        const float lo = fminf(T[i], T[j]), hi = fmaxf(T[i], T[j]);
-        T[i] = lo;
-        T[j] = hi;
-      }
-    }
-  }
-}
 
 // merge the lane's new log entries into F (all lanes in lockstep: max(new) rounds)
 template <int K, bool LB>
@@ -432,9 +389,8 @@ __device__ __forceinline__ void eval_block(WarpBuf<K> &B, int n, float qx, float
       if (__any_sync(0xffffffffu, L.nl > C - 8)) compact<K, LB>(B, L);
     }
   }
-  // refresh the k-th value for the next pruning decisions once some lane has enough new
-  // entries (merge rounds = max new entries over the lanes)
-  if (__any_sync(0xffffffffu, L.nl - L.nf >= JZ_MERGE_MIN)) merge<K, LB>(B, L);
+  // refresh the k-th value for the next pruning decisions (merge rounds = max new entries)
+  merge<K, LB>(B, L);
 }
 
 // pad a staged batch [0, n) (n multiple of 4) with NaN sources to a multiple of 8
@@ -565,9 +521,7 @@ __device__ __forceinline__ void visit_leaves(const LeafPK &a, const Dom &D, Warp
         }
         nev += act ? (unsigned)m : 0u;
         JZ_DIAG(4, 1);
-#ifndef JZ_DIAG_OWN
         ++L.stg;
-#endif
         n += (m + 3) & ~3;
       }
       if (n == 0) continue;
@@ -629,18 +583,16 @@ __device__ __forceinline__ void bitonic_sort_f(float (&T)[K]) {
   }
 }
 
-#ifndef JZ_WIN2
-#define JZ_WIN2 0
-#endif
-// window width: 2K sources for K <= 16 (the K smallest of them start the list), K for K = 32
+// window width: K sources (a 2K window with the K smallest kept cut insertions 26 -> 15 per
+// query but cost more than it saved)
 template <int K>
 struct WinN {
-  static constexpr int N = (JZ_WIN2 && K <= 16) ? 2 * K : K;
+  static constexpr int N = K;
 };
 
 // z-window initialisation (self-query): the N = WinN<K>::N sources at sorted positions
 // [wpos, wpos + N) around the lane's own query are evaluated first; their keys start the log
-// and the K smallest values the list, so the k-th value is already close before the own
+// and their sorted values the list, so the k-th value is already close before the own
 // leaves are scanned (z-order neighbours are mostly spatial neighbours, P:L69 / Fig. 2).
 template <int K, bool LB, bool PER>
 __device__ __forceinline__ void window_init(const LeafPK &a, const Dom &D, WarpBuf<K> &B, int wpos, float qx,
@@ -648,7 +600,7 @@ __device__ __forceinline__ void window_init(const LeafPK &a, const Dom &D, WarpB
   constexpr int N = WinN<K>::N;
   static_assert(N <= LogCap<K>::C, "the window must fit the log");
   const int lane = threadIdx.x & 31;
-  float W0[K], W1[K];
+  float W[K];
 #pragma unroll
   for (int o = 0; o < N; ++o) {
     float d = INFINITY;
@@ -658,22 +610,14 @@ __device__ __forceinline__ void window_init(const LeafPK &a, const Dom &D, WarpB
       B.ld[o][lane] = __float_as_uint(d);
       B.lg[o][lane] = (unsigned)(__float_as_int(p.w) + 1);
     }
-    if (o < K) W0[o] = d;
-    else W1[o - K < K ? o - K : 0] = d;
+    W[o] = d;
   }
-  bitonic_sort_f<K>(W0);
-  if (N > K) {
-    bitonic_sort_f<K>(W1);
+  bitonic_sort_f<K>(W);
 #pragma unroll
-    for (int i = 0; i < K; ++i) W0[i] = fminf(W0[i], W1[K - 1 - i]);  // K smallest of the 2K, bitonic
-    bitonic_merge_f<K>(W0);
-  }
-#pragma unroll
-  for (int j = 0; j < K; ++j) L.F[j] = W0[j];
+  for (int j = 0; j < K; ++j) L.F[j] = W[j];
   L.nl = L.nf = act ? N : 0;
   L.app += act ? N : 0;
   L.kth = act ? L.F[K - 1] : -1.f;
-  if (N > K) compact<K, LB>(B, L);  // keep the entries <= the k-th value
 }
 
 // pre-pass over the warp's own sources [s0, s1) (the sources of the leaves holding its
@@ -792,10 +736,6 @@ __global__ void __launch_bounds__(kLThreads, MinBlocks<K>::v) k_leaf(LeafPK a, D
     }
     L.stg += xb - xa;
     own_pass<K, LB, PER>(a, D, B, s0o, s1o, cls_all, wpos, qx, qy, qz, act, L, nev);
-    if (JZ_MERGE_MIN > 1) merge<K, LB>(B, L);
-#ifdef JZ_DIAG_OWN
-    L.stg = L.rnd * 1000u + __reduce_add_sync(0xffffffffu, L.app);  // diagnostics: rounds, appends after the own pass
-#endif
   }
   const int64_t eb = a.ispl[J], ee = a.ispl[J + 1];
   // entries in chunks of 32, one lane per entry (list order = r_low order): the node tests run in
