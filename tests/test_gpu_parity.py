@@ -524,3 +524,37 @@ def test_fof_c4_distribution_full():
     label vs the grid oracle."""
     pos, box, _ = make_config("C4", n=1_000_000)
     _fof_cmp(pos, 0.2 * 1e6 ** (-1 / 3), box, min_count=20)
+
+
+# ----------------------------------------------------------------------------------- edge cases
+@pytest.mark.parametrize("n,k,box", [(1, 1, 1.0), (2, 2, None), (3, 1, 1.0), (40, 40, 1.0), (33, 33, None),
+                                     (100, 64, 1.0), (257, 8, None)])
+def test_tiny_and_k_equals_n(n, k, box):
+    """Degenerate sizes: one point, k = n (every point in every row, including k > 32 = k_max
+    passes), a ragged tail of the 32-query work items."""
+    pos = uniform_points(n, 300 + n, 1.0)
+    ig, dg = _gpu_knn(pos, k, box)
+    io, do = knn_brute(pos, k, box)
+    _assert_same(ig, dg, io, do)
+
+
+@pytest.mark.parametrize("offset,scale", [(1.0e6, 1.0), (-3.0e5, 50.0), (1.0e-3, 1.0e-6)])
+def test_far_offsets_and_tiny_scales(offset, scale):
+    """Open domain far from the origin (coordinates ~1e6 with unit spread: FP32 spacing ~0.06) and
+    a microscopic cloud: the rounding margins of the pruning bounds (R8b) must keep every
+    true neighbour."""
+    pos = (uniform_points(20000, 310, 1.0).astype(np.float64) * scale + offset).astype(np.float32)
+    ig, dg = _gpu_knn(pos, 16, None)
+    io, do = knn_brute(pos, 16, None)
+    _assert_same(ig, dg, io, do)
+
+
+def test_periodic_points_near_the_box_faces():
+    """Periodic box with most points within 1e-4 of the faces: every leaf pair straddles or wraps
+    (per-pair select and shift classes, R8b)."""
+    p = uniform_points(30000, 311, 1.0).astype(np.float64)
+    p = np.where(p < 0.5, p * 2e-4, 1.0 - (1.0 - p) * 2e-4).astype(np.float32)
+    p[p >= np.float32(1.0)] = np.float32(0.0)  # float32 rounding can reach L
+    ig, dg = _gpu_knn(p, 16, 1.0)
+    io, do = knn_grid(p, 16, 1.0)
+    _assert_same(ig, dg, io, do)
