@@ -61,9 +61,12 @@ template <int K>
 struct LogCap {
   static constexpr int C = K + (K > 16 ? JZ_LOGX32 : JZ_LOGX);  // log entries per lane
 };
+#ifndef JZ_MINB8
+#define JZ_MINB8 JZ_MINB
+#endif
 template <int K>
 struct MinBlocks {
-  static constexpr int v = K > 16 ? JZ_MINB32 : JZ_MINB;  // CTAs per SM the register budget targets
+  static constexpr int v = K > 16 ? JZ_MINB32 : (K <= 8 ? JZ_MINB8 : JZ_MINB);  // CTAs per SM the register budget targets
 };
 
 typedef unsigned long long u64;
