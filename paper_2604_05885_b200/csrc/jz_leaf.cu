@@ -167,10 +167,6 @@ __global__ void k_box_ce(const NodeBox *__restrict__ box, int64_t n, float Lmax,
   }
 }
 
-// ---------------------------------------------------------------- top-k state
-// insert value d into the sorted list F, dropping the largest (identity when d >= F[K-1]):
-// F'[j] = max(F[j-1], min(F[j], d)), F'[0] = min(F[0], d) -- every slot independent (depth 2,
-// no serial chain). Warp-converged: the lower half runs only when some lane's d lands there.
 // insert value d into the sorted list F, dropping the largest (identity when d >= F[K-1]):
 // F'[j] = max(F[j-1], min(F[j], d)), F'[0] = min(F[0], d) -- every slot independent (depth 2, no
 // serial chain); the lower half runs only when some lane's d lands there (late insertions land
@@ -184,6 +180,21 @@ __device__ __forceinline__ void bubble(float (&F)[K], float d) {
 #pragma unroll
     for (int j = J0 - 1; j > 0; --j) F[j] = fmaxf(F[j - 1], fminf(F[j], d));
     F[0] = fminf(F[0], d);
+  }
+}
+
+// insert two values a <= b at once: F'[j] = max(F[j-2], min(F[j-1], b), min(F[j], a)) (the
+// (j+1)-th smallest of F, a, b), 3 instructions per slot for two insertions; same gating.
+template <int K>
+__device__ __forceinline__ void bubble2(float (&F)[K], float a, float b) {
+  constexpr int J0 = K / 2;
+#pragma unroll
+  for (int j = K - 1; j >= J0 && j > 1; --j) F[j] = fmaxf(fmaxf(F[j - 2], fminf(F[j - 1], b)), fminf(F[j], a));
+  if (__any_sync(0xffffffffu, a < F[J0 > 0 ? J0 - 1 : 0])) {
+#pragma unroll
+    for (int j = J0 - 1; j > 1; --j) F[j] = fmaxf(fmaxf(F[j - 2], fminf(F[j - 1], b)), fminf(F[j], a));
+    if (K > 1) F[1] = fmaxf(fminf(F[0], b), fminf(F[1], a));
+    F[0] = fminf(F[0], a);
   }
 }
 
@@ -224,15 +235,15 @@ __device__ __forceinline__ void merge(WarpBuf<K> &B, Lane<K, LB> &L) {
   const int lane = threadIdx.x & 31;
   const int nr = (int)__reduce_max_sync(0xffffffffu, (unsigned)(L.nl - L.nf));
   if (JZ_STATS) L.rnd += nr;
-  unsigned nx = L.nf < L.nl ? B.ld[L.nf][lane] : 0x7f800000u;
 #pragma unroll 1
-  for (int i = 0; i < nr; ++i) {
+  for (int i = 0; i < nr; i += 2) {  // two entries per round
     const int r = L.nf + i;
-    const float d = __uint_as_float(nx);
-    nx = r + 1 < L.nl ? B.ld[r + 1][lane] : 0x7f800000u;  // prefetch the next round's entry
-    const bool in = d < L.F[K - 1];
-    if (__any_sync(0xffffffffu, in)) bubble<K>(L.F, d);
-    if (JZ_STATS) L.ins += in;
+    const float d1 = __uint_as_float(r < L.nl ? B.ld[r][lane] : 0x7f800000u);
+    const float d2 = __uint_as_float(r + 1 < L.nl ? B.ld[r + 1][lane] : 0x7f800000u);
+    const float lo = fminf(d1, d2), hi = fmaxf(d1, d2);
+    const bool in = lo < L.F[K - 1];
+    if (__any_sync(0xffffffffu, in)) bubble2<K>(L.F, lo, hi);
+    if (JZ_STATS) L.ins += in + (hi < L.F[K - 1]);
   }
   L.nf = L.nl;
   L.kth = L.act ? L.F[K - 1] : -1.f;
