@@ -210,8 +210,7 @@ template <int K>
 struct WarpBuf {
   float x[kLCap + 8], y[kLCap + 8], z[kLCap + 8];  // + 8: padding to a multiple of 8
   int g[kLCap + 8];
-  unsigned ld[LogCap<K>::C][32];  // log: d2 bits (lane-minor: conflict-free)
-  unsigned lg[LogCap<K>::C][32];  // log: gidx + 1
+  u64 lk[LogCap<K>::C][32];  // log: keys d2_bits << 32 | gidx + 1 (lane-minor: conflict-free)
 };
 
 template <int K, bool LB>
@@ -238,8 +237,8 @@ __device__ __forceinline__ void merge(WarpBuf<K> &B, Lane<K, LB> &L) {
 #pragma unroll 1
   for (int i = 0; i < nr; i += 2) {  // two entries per round
     const int r = L.nf + i;
-    const float d1 = __uint_as_float(r < L.nl ? B.ld[r][lane] : 0x7f800000u);
-    const float d2 = __uint_as_float(r + 1 < L.nl ? B.ld[r + 1][lane] : 0x7f800000u);
+    const float d1 = __uint_as_float(r < L.nl ? (unsigned)(B.lk[r][lane] >> 32) : 0x7f800000u);
+    const float d2 = __uint_as_float(r + 1 < L.nl ? (unsigned)(B.lk[r + 1][lane] >> 32) : 0x7f800000u);
     const float lo = fminf(d1, d2), hi = fmaxf(d1, d2);
     const bool in = lo < L.F[K - 1];
     if (__any_sync(0xffffffffu, in)) bubble2<K>(L.F, lo, hi);
@@ -258,14 +257,13 @@ __device__ __noinline__ int drop_largest(WarpBuf<K> &B, int nl, int keep) {
     int im = 0;
     u64 mk = 0;
     for (int r = 0; r < nl; ++r) {
-      const u64 e = ((u64)B.ld[r][lane] << 32) | B.lg[r][lane];
+      const u64 e = B.lk[r][lane];
       if (e > mk) {
         mk = e;
         im = r;
       }
     }
-    B.ld[im][lane] = B.ld[nl - 1][lane];
-    B.lg[im][lane] = B.lg[nl - 1][lane];
+    B.lk[im][lane] = B.lk[nl - 1][lane];
     --nl;
   }
   return nl;
@@ -282,21 +280,13 @@ __device__ __forceinline__ void compact(WarpBuf<K> &B, Lane<K, LB> &L) {
   int j = 0;
 #pragma unroll 1
   for (int r = 0; r < r1; r += 4) {  // 4 independent loads per step
-    unsigned d[4], g[4];
+    u64 e[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) e[u] = r + u < L.nl ? B.lk[r + u][lane] : ~0ull;
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      d[u] = 0xffffffffu;
-      g[u] = 0;
-      if (r + u < L.nl) {
-        d[u] = B.ld[r + u][lane];
-        g[u] = B.lg[r + u][lane];
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      if (d[u] <= kb) {  // 0xffffffff (no entry) never passes: kb <= 0x7f800000 or inactive
-        B.ld[j][lane] = d[u];
-        B.lg[j][lane] = g[u];
+      if ((unsigned)(e[u] >> 32) <= kb) {  // ~0 (no entry) never passes: kb <= 0x7f800000 or inactive
+        B.lk[j][lane] = e[u];
         ++j;
       }
     }
@@ -310,8 +300,7 @@ __device__ __forceinline__ void append(WarpBuf<K> &B, Lane<K, LB> &L, float d2, 
   if (d2 <= L.kth) {
     const u64 key = ((u64)__float_as_uint(d2) << 32) | (unsigned)(g + 1);
     if (!LB || key > L.lb) {
-      B.ld[L.nl][threadIdx.x & 31] = __float_as_uint(d2);
-      B.lg[L.nl][threadIdx.x & 31] = (unsigned)(g + 1);
+      B.lk[L.nl][threadIdx.x & 31] = key;
       ++L.nl;
       if (JZ_STATS) ++L.app;
     }
@@ -621,8 +610,7 @@ __device__ __forceinline__ void window_init(const LeafPK &a, const Dom &D, WarpB
     if (act) {
       const float4 p = a.spts[wpos + o];
       d = PER ? canon_d2_per(qx, qy, qz, p.x, p.y, p.z, D) : canon_d2_open(qx, qy, qz, p.x, p.y, p.z);
-      B.ld[o][lane] = __float_as_uint(d);
-      B.lg[o][lane] = (unsigned)(__float_as_int(p.w) + 1);
+      B.lk[o][lane] = ((u64)__float_as_uint(d) << 32) | (unsigned)(__float_as_int(p.w) + 1);
     }
     W[o] = d;
   }
@@ -809,7 +797,7 @@ __global__ void __launch_bounds__(kLThreads, MinBlocks<K>::v) k_leaf(LeafPK a, D
   if (act) {
     u64 T[K];
 #pragma unroll
-    for (int j = 0; j < K; ++j) T[j] = j < L.nl ? (((u64)B.ld[j][lane] << 32) | B.lg[j][lane]) : ~0ull;
+    for (int j = 0; j < K; ++j) T[j] = j < L.nl ? B.lk[j][lane] : ~0ull;
     bitonic_sort<K>(T);
     int32_t *oi = a.out_idx + row * a.ldo + a.col0;
     float *od = a.out_d2 + row * a.ldo + a.col0;
