@@ -60,8 +60,9 @@ enum {
   JZ_FLAG_FRAME = 1u << 0,         /* use frame_origin / frame_extent for the Morton keys (multi-GPU: one global frame) */
   JZ_FLAG_NO_EARLY_EXIT = 1u << 1, /* disable the sorted-r_low early exit (pruning-safety tests) */
   JZ_FLAG_NO_SEGSORT = 1u << 2,    /* do not sort interaction segments by r_low (implies no early exit) */
-  JZ_FLAG_QBOX_WALK = 1u << 3      /* jz_knn_query_boxes: R_max by the NodeToNode walk to the leaf plane
-                                      instead of the smallest-ancestor diagonal (tighter, ~5x slower) */
+  JZ_FLAG_QBOX_DIAG = 1u << 3      /* jz_knn_query_boxes: R_max = AABB diagonal of the smallest ancestor
+                                      holding k points instead of the NodeToNode walk (no walk, but far
+                                      looser on clustered data: measured 7x more ghosts) */
 };
 
 /* Tree / walk parameters. Zero fields take the defaults (nmax0 see DESIGN.md §6). */
@@ -201,9 +202,9 @@ JZ_API int jz_knn_plane_nodes(const jz_knn_index *ix, int plane, int64_t *nnodes
 
 /* Query boxes for ghost selection: for each node of `plane` (< 0: top plane), its AABB
  * and the largest R_max^2 of its leaves; R_max^2 bounds the canonical k-th neighbour d2
- * of every contained query point. Default: the AABB diagonal (self d_up^2, exact R8 bound) of
- * the smallest ancestor-or-self node holding >= k points -- it contains k candidates -- with no
- * walk; with JZ_FLAG_QBOX_WALK: FindRmax down to the leaf plane, tighter boxes.
+ * of every contained query point: FindRmax down to the leaf plane; with
+ * JZ_FLAG_QBOX_DIAG the AABB diagonal (self d_up^2, exact R8 bound) of the smallest
+ * ancestor-or-self node holding >= k points (no walk, looser).
  * boxes [nnodes][8] floats {lo.x, lo.y, lo.z, r2, hi.x, hi.y, hi.z, bits(rank)} (device). */
 JZ_API int jz_knn_query_boxes(jz_knn_index *ix, int k, int plane, int rank, float *boxes, jz_stream_t s);
 

@@ -14,7 +14,7 @@ LIB_PATH = os.path.join(_HERE, "libjzknn.so")
 
 JZ_OK, JZ_EINVAL, JZ_EDATA, JZ_ECAPACITY, JZ_ECUDA, JZ_ENOMEM = 0, 2, 3, 4, 5, 7
 JZ_ORDER_INPUT, JZ_ORDER_Z = 0, 1
-JZ_FLAG_FRAME, JZ_FLAG_NO_EARLY_EXIT, JZ_FLAG_NO_SEGSORT, JZ_FLAG_QBOX_WALK = 1, 2, 4, 8
+JZ_FLAG_FRAME, JZ_FLAG_NO_EARLY_EXIT, JZ_FLAG_NO_SEGSORT, JZ_FLAG_QBOX_DIAG = 1, 2, 4, 8
 
 # every symbol include/jz_knn.h declares (tests check the library exports them all)
 EXPORTS = [

@@ -6,8 +6,8 @@
 //   jz_bucket_by_splitters  dest rank = #splitters <= key (Morton-range partition)
 //   jz_pack_by_rank         float4 {x, y, z, bits(gidx)} grouped by destination rank
 //   jz_knn_query_boxes      per node of a plane: AABB + max R_max^2 of its leaves (default: the
-//                           AABB diagonal of the smallest ancestor holding k points; with
-//                           JZ_FLAG_QBOX_WALK the NodeToNode walk to the leaf plane, Alg. 1 l. 1-5)
+//                           NodeToNode walk to the leaf plane, Alg. 1 l. 1-5; JZ_FLAG_QBOX_DIAG:
+//                           the AABB diagonal of the smallest ancestor holding k points)
 //   jz_knn_select_ghosts    bitmask of peer ranks whose query boxes a local leaf reaches
 //                           (exact monotone box bound d_low^2 <= r2; leaf granularity is a
 //                           superset of the required points, so no neighbour can be missed)
@@ -174,9 +174,11 @@ __device__ __forceinline__ NodeBox qbox_at(const float *__restrict__ q, int64_t 
 }
 
 constexpr int kGhostCand = 2048;
+constexpr int kGhostHit = 16;  // query boxes per leaf kept for the point-level filter
 
 // one CTA per node of the top plane: candidate peer boxes, then its leaves
-__global__ void __launch_bounds__(256) k_select_ghosts(const NodeBox *__restrict__ topbox,
+__global__ void __launch_bounds__(256) k_select_ghosts(const float4 *__restrict__ pts,
+                                                       const NodeBox *__restrict__ topbox,
                                                        const int32_t *__restrict__ top_leafspl,
                                                        const NodeBox *__restrict__ leafbox,
                                                        const int32_t *__restrict__ leafbeg, const float *__restrict__ qb,
@@ -214,6 +216,8 @@ __global__ void __launch_bounds__(256) k_select_ghosts(const NodeBox *__restrict
   for (int l = top_leafspl[T] + threadIdx.x; l < top_leafspl[T + 1]; l += blockDim.x) {
     const NodeBox lb = leafbox[l];
     int m = 0;
+    int hit[kGhostHit];  // query boxes reaching this leaf (point-level filter below)
+    int nh = 0;
     const int64_t lim = over ? nqb : nc;
     for (int64_t c = 0; c < lim; ++c) {
       const int64_t j = over ? c : s_cand[c];
@@ -221,9 +225,32 @@ __global__ void __launch_bounds__(256) k_select_ghosts(const NodeBox *__restrict
       int rk;
       const NodeBox b = qbox_at(qb, j, &r2, &rk);
       if (rk == self || rk < 0 || rk > 31) continue;
-      if (box_dlow2(lb, b, D) <= r2) m |= 1 << rk;
+      if (box_dlow2(lb, b, D) <= r2) {
+        m |= 1 << rk;
+        if (nh < kGhostHit) hit[nh] = (int)j;
+        ++nh;
+      }
     }
-    for (int i = leafbeg[l]; i < leafbeg[l + 1]; ++i) mask[i] = m;
+    if (m == 0 || nh > kGhostHit) {  // nothing, or too many boxes: leaf granularity
+      for (int i = leafbeg[l]; i < leafbeg[l + 1]; ++i) mask[i] = m;
+      continue;
+    }
+    // point granularity: a point goes to rank r only if one of r's boxes reaches the point itself
+    // (exact point-box bound, the same test as the box test with a degenerate box)
+    for (int i = leafbeg[l]; i < leafbeg[l + 1]; ++i) {
+      const float4 p = pts[i];
+      NodeBox pb;
+      pb.lo = make_float4(p.x, p.y, p.z, 0.f);
+      pb.hi = pb.lo;
+      int pm = 0;
+      for (int h = 0; h < nh; ++h) {
+        float r2;
+        int rk;
+        const NodeBox b = qbox_at(qb, hit[h], &r2, &rk);
+        if (!((pm >> rk) & 1) && box_dlow2(pb, b, D) <= r2) pm |= 1 << rk;
+      }
+      mask[i] = pm;
+    }
   }
 }
 
@@ -397,11 +424,11 @@ int jz_knn_query_boxes(jz_knn_index *ix, int k, int plane, int rank, float *boxe
       std::vector<float> inf(pl[0].nnodes, INFINITY);
       JZ_CUDA(cudaMemcpyAsync(rmax2, inf.data(), inf.size() * sizeof(float), cudaMemcpyHostToDevice, st));
       JZ_CUDA(cudaStreamSynchronize(st));
-    } else if (v.flags & JZ_FLAG_QBOX_WALK) {  // R_max from the NodeToNode walk to the leaf plane (tighter, slower)
+    } else if (!(v.flags & JZ_FLAG_QBOX_DIAG)) {  // default: R_max from the NodeToNode walk to the leaf plane
       int32_t *sb = nullptr;
       jz::walk_to(pl, v.D, k, v.ngr, v.flags, 0, il, &rmax2, &sb, st);
       il.release(st);
-    } else {  // default: the diagonal of the smallest ancestor holding k points (no walk)
+    } else {  // the diagonal of the smallest ancestor holding k points (no walk; far looser on clustered data)
       const int nup = (int)pl.size() - 1;
       std::vector<jz::PlaneRef> h(nup > 0 ? nup : 1);
       for (int p = 1; p < (int)pl.size(); ++p) h[p - 1] = jz::PlaneRef{pl[p].leafspl, pl[p].box, pl[p].nnodes};
@@ -435,7 +462,7 @@ int jz_knn_select_ghosts(jz_knn_index *ix, const float *boxes, int64_t nbox, int
     const int top = (int)pl.size() - 1;
     JZ_CUDA(cudaMemsetAsync(counts, 0, nranks * sizeof(int64_t), st));
     if (nbox > 0) {
-      jz::k_select_ghosts<<<(unsigned)pl[top].nnodes, 256, 0, st>>>(pl[top].box, pl[top].leafspl, pl[0].box,
+      jz::k_select_ghosts<<<(unsigned)pl[top].nnodes, 256, 0, st>>>(v.pts, pl[top].box, pl[top].leafspl, pl[0].box,
                                                                      pl[0].beg, boxes, nbox, self_rank, v.D, mask);
       JZ_LAUNCH_CHECK();
       jz::k_ghost_count<<<jz::grid_for(v.n, 256, 148 * 4), 256, 0, st>>>(mask, v.n, nranks,

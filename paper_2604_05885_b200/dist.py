@@ -34,6 +34,7 @@ import numpy as np
 import torch
 
 N_SAMP = 1000
+QBOX_NODES = int(__import__('os').environ.get('JZ_QBOX_NODES', '4096'))  # query-box plane size cap
 
 
 # ----------------------------------------------------------------------------- comms
@@ -229,13 +230,13 @@ class GpuBackend:
     def query_boxes(self, ix, k, rank):
         import ctypes
 
-        # finest plane with at most 4096 nodes (peers test every box against their top nodes)
+        # finest plane with at most QBOX_NODES nodes (peers test every box against their top nodes)
         nn = ctypes.c_int64()
         P = ix.num_planes()
         plane = P - 1
         for p in range(P):
             self.B.check(self.lib.jz_knn_plane_nodes(ix.handle(), p, ctypes.byref(nn)))
-            if nn.value <= 4096:
+            if nn.value <= QBOX_NODES:
                 plane = p
                 break
         self.B.check(self.lib.jz_knn_plane_nodes(ix.handle(), plane, ctypes.byref(nn)))
