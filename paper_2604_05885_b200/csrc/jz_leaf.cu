@@ -33,13 +33,16 @@
 
 namespace jz {
 
-constexpr int kLWarps = 2;
+#ifndef JZ_LWARPS
+#define JZ_LWARPS 1  // one work item per CTA: CTAs retire independently (2 warps: 132.5 ms, 1: 127.0 ms)
+#endif
+constexpr int kLWarps = JZ_LWARPS;  // warps (independent work items) per LeafToLeaf CTA
 constexpr int kLThreads = kLWarps * 32;
 #ifndef JZ_LCAP
 #define JZ_LCAP 128
 #endif
 #ifndef JZ_MINB
-#define JZ_MINB 9  // 9 CTAs x 2 warps per SM: 96 registers (5 warps per SM partition; smem allows 9 CTAs at K = 16)
+#define JZ_MINB 18  // 18 one-warp CTAs per SM: 96 registers (5 warps per SM partition; smem allows 18 at K = 16)
 #endif
 constexpr int kLCap = JZ_LCAP;  // staged source points per warp (2 KB SoA); >= the largest leaf (kMaxLeaf)
 static_assert(JZ_LCAP >= kMaxLeaf, "a leaf must fit the staging buffer");
@@ -55,7 +58,7 @@ static_assert(JZ_LCAP >= kMaxLeaf, "a leaf must fit the staging buffer");
 #define JZ_LOGX32 16  // K = 32: 48-entry log (14 KB per warp with staging) -> 7 CTAs per SM
 #endif
 #ifndef JZ_MINB32
-#define JZ_MINB32 7  // K = 32: 144 registers, no spills (the K = 16 budget of 96 spilled: C3 48 -> 33 ms)
+#define JZ_MINB32 14  // K = 32: 144 registers, no spills (the K = 16 budget of 96 spilled: C3 48 -> 33 ms)
 #endif
 template <int K>
 struct LogCap {
