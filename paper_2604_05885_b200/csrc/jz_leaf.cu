@@ -48,7 +48,7 @@ constexpr int kLCap = JZ_LCAP;  // staged source points per warp (2 KB SoA); >= 
 static_assert(JZ_LCAP >= kMaxLeaf, "a leaf must fit the staging buffer");
 
 #ifndef JZ_LOGX
-#define JZ_LOGX 24
+#define JZ_LOGX 16  // K = 16: 32-entry log (10 KB per one-warp CTA with staging)
 #endif
 #ifndef JZ_STATS
 #define JZ_STATS 1  // per-lane walk counters (appends, merge rounds, compactions, staged leaves)

@@ -112,7 +112,10 @@ __device__ __forceinline__ void heap_insert(CountHeap &h, float r, int c, int k)
 // One warp per receiving parent (4 parents per CTA), one lane per child; the source
 // parent's children are staged in the warp's shared-memory slot. Warps are independent
 // (no CTA barriers); the RMAX early exit is a warp vote.
-constexpr int kN2NWarps = 4;
+#ifndef JZ_N2N_WARPS
+#define JZ_N2N_WARPS 1
+#endif
+constexpr int kN2NWarps = JZ_N2N_WARPS;
 constexpr int kN2NWStage = 128;  // staged source children per warp (4 KB)
 
 template <int MODE>
