@@ -219,8 +219,15 @@ __global__ void k_fof_flatten(int32_t *__restrict__ par, int64_t n) {
 }
 __global__ void k_fof_minlab(const float4 *__restrict__ pts, const int32_t *__restrict__ par, int64_t n,
                              int32_t *__restrict__ minlab) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    atomicMin(&minlab[par[i]], __float_as_int(pts[i].w));
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n; i0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = i0 + threadIdx.x;
+    const bool ok = i < n;
+    const int32_t r = ok ? par[i] : -1;
+    const int g = ok ? __float_as_int(pts[i].w) : INT32_MAX;
+    const unsigned peers = __match_any_sync(0xffffffffu, r);
+    const int gm = __reduce_min_sync(peers, g);  // one atomic per (warp, group)
+    if (ok && (threadIdx.x & 31) == __ffs(peers) - 1) atomicMin(&minlab[r], gm);
+  }
 }
 // label of input row gidx = smallest input index of its group (R21)
 __global__ void k_fof_labels(const float4 *__restrict__ pts, const int32_t *__restrict__ par,
@@ -233,27 +240,77 @@ __device__ __forceinline__ double fof_disp(float x, float xr, int periodic, floa
   if (periodic) d -= (double)L * rint(d / (double)L);  // minimal image w.r.t. the group's root point
   return d;
 }
-__global__ void k_fof_sum1(const float4 *__restrict__ pts, const int32_t *__restrict__ par, int64_t n, jz::Dom D,
-                           int32_t *__restrict__ cnt, double *__restrict__ sum) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t r = par[i];
-    const float4 p = pts[i], q = pts[r];
-    atomicAdd(&cnt[r], 1);
-    atomicAdd(&sum[3 * (int64_t)r + 0], fof_disp(p.x, q.x, D.periodic, D.L[0]));
-    atomicAdd(&sum[3 * (int64_t)r + 1], fof_disp(p.y, q.y, D.periodic, D.L[1]));
-    atomicAdd(&sum[3 * (int64_t)r + 2], fof_disp(p.z, q.z, D.periodic, D.L[2]));
+// Per-group sums with one set of atomics per (warp, group): consecutive z positions mostly share
+// a root, so the lanes of a group put their values in shared memory and the group's first lane
+// adds them up (a group of 10^5 points would otherwise serialise 10^5 FP64 atomics on one address).
+constexpr int kFofThreads = 256;
+__global__ void __launch_bounds__(kFofThreads) k_fof_sum1(const float4 *__restrict__ pts,
+                                                          const int32_t *__restrict__ par, int64_t n, jz::Dom D,
+                                                          int32_t *__restrict__ cnt, double *__restrict__ sum) {
+  __shared__ double s_v[kFofThreads][3];
+  const int lane = threadIdx.x & 31, wb = threadIdx.x & ~31;
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n; i0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = i0 + threadIdx.x;
+    const bool ok = i < n;
+    int32_t r = -1;
+    double dx = 0.0, dy = 0.0, dz = 0.0;
+    if (ok) {
+      r = par[i];
+      const float4 p = pts[i], q = pts[r];
+      dx = fof_disp(p.x, q.x, D.periodic, D.L[0]);
+      dy = fof_disp(p.y, q.y, D.periodic, D.L[1]);
+      dz = fof_disp(p.z, q.z, D.periodic, D.L[2]);
+    }
+    s_v[threadIdx.x][0] = dx;
+    s_v[threadIdx.x][1] = dy;
+    s_v[threadIdx.x][2] = dz;
+    const unsigned peers = __match_any_sync(0xffffffffu, r);
+    __syncwarp();
+    if (ok && lane == __ffs(peers) - 1) {
+      double a = 0.0, b = 0.0, c = 0.0;
+      for (unsigned m = peers; m; m &= m - 1) {
+        const int t = wb + __ffs(m) - 1;
+        a += s_v[t][0];
+        b += s_v[t][1];
+        c += s_v[t][2];
+      }
+      atomicAdd(&cnt[r], __popc(peers));
+      atomicAdd(&sum[3 * (int64_t)r + 0], a);
+      atomicAdd(&sum[3 * (int64_t)r + 1], b);
+      atomicAdd(&sum[3 * (int64_t)r + 2], c);
+    }
+    __syncwarp();
   }
 }
-__global__ void k_fof_sum2(const float4 *__restrict__ pts, const int32_t *__restrict__ par, int64_t n, jz::Dom D,
-                           const int32_t *__restrict__ cnt, const double *__restrict__ sum, double *__restrict__ ss) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t r = par[i];
-    const float4 p = pts[i], q = pts[r];
-    const double c = (double)cnt[r];
-    const double dx = fof_disp(p.x, q.x, D.periodic, D.L[0]) - sum[3 * (int64_t)r] / c;
-    const double dy = fof_disp(p.y, q.y, D.periodic, D.L[1]) - sum[3 * (int64_t)r + 1] / c;
-    const double dz = fof_disp(p.z, q.z, D.periodic, D.L[2]) - sum[3 * (int64_t)r + 2] / c;
-    atomicAdd(&ss[r], dx * dx + dy * dy + dz * dz);
+__global__ void __launch_bounds__(kFofThreads) k_fof_sum2(const float4 *__restrict__ pts,
+                                                          const int32_t *__restrict__ par, int64_t n, jz::Dom D,
+                                                          const int32_t *__restrict__ cnt,
+                                                          const double *__restrict__ sum, double *__restrict__ ss) {
+  __shared__ double s_v[kFofThreads];
+  const int lane = threadIdx.x & 31, wb = threadIdx.x & ~31;
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n; i0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = i0 + threadIdx.x;
+    const bool ok = i < n;
+    int32_t r = -1;
+    double v = 0.0;
+    if (ok) {
+      r = par[i];
+      const float4 p = pts[i], q = pts[r];
+      const double c = (double)cnt[r];
+      const double dx = fof_disp(p.x, q.x, D.periodic, D.L[0]) - sum[3 * (int64_t)r] / c;
+      const double dy = fof_disp(p.y, q.y, D.periodic, D.L[1]) - sum[3 * (int64_t)r + 1] / c;
+      const double dz = fof_disp(p.z, q.z, D.periodic, D.L[2]) - sum[3 * (int64_t)r + 2] / c;
+      v = dx * dx + dy * dy + dz * dz;
+    }
+    s_v[threadIdx.x] = v;
+    const unsigned peers = __match_any_sync(0xffffffffu, r);
+    __syncwarp();
+    if (ok && lane == __ffs(peers) - 1) {
+      double a = 0.0;
+      for (unsigned m = peers; m; m &= m - 1) a += s_v[wb + __ffs(m) - 1];
+      atomicAdd(&ss[r], a);
+    }
+    __syncwarp();
   }
 }
 __global__ void k_fof_flags(const int32_t *__restrict__ par, const int32_t *__restrict__ cnt, int64_t n, int min_count,
@@ -585,9 +642,9 @@ int jz_fof(jz_knn_index *ix, float r_link, int32_t min_count, int32_t *labels, i
   JZ_CUDA(cudaMemsetAsync(cnt, 0, n * sizeof(int32_t), st));
   JZ_CUDA(cudaMemsetAsync(sum, 0, 3 * n * sizeof(double), st));
   JZ_CUDA(cudaMemsetAsync(ss, 0, n * sizeof(double), st));
-  k_fof_sum1<<<jz::grid_for(n, 256), 256, 0, st>>>(ix->pts, par, n, ix->D, cnt, sum);
+  k_fof_sum1<<<jz::grid_for(n, kFofThreads), kFofThreads, 0, st>>>(ix->pts, par, n, ix->D, cnt, sum);
   JZ_LAUNCH_CHECK();
-  k_fof_sum2<<<jz::grid_for(n, 256), 256, 0, st>>>(ix->pts, par, n, ix->D, cnt, sum, ss);
+  k_fof_sum2<<<jz::grid_for(n, kFofThreads), kFofThreads, 0, st>>>(ix->pts, par, n, ix->D, cnt, sum, ss);
   JZ_LAUNCH_CHECK();
   k_fof_flags<<<jz::grid_for(n, 256), 256, 0, st>>>(par, cnt, n, min_count, flag);
   JZ_LAUNCH_CHECK();
