@@ -251,10 +251,22 @@ static inline void scan_cell(const grid_t *g, const float *pos, const float *q, 
  * Grid shell search. After finishing Chebyshev shell s around the query's cell
  * the visited region is the cube of cells [c-s, c+s]^3 (wrapped when periodic).
  * r_s = distance (float64) from q to the outside of that cube, minus a slack
- * of 1e-12 * extent. Stop once cnt == k and d2_k < r_s^2 (1 - 1e-6): any
- * unvisited point has exact d2 >= r_s^2 and canonical FP32 d2 >= exact d2
- * (1 - 6 * 2^-24) > d2_k, so it cannot enter the list (not even on a tie).
- * Also stop once every cell has been visited.
+ * of 1e-12 * extent, minus (periodic only) the wrap slack sqrt(3) * 2^-24 * L_max.
+ * Stop once cnt == k and d2_k < r_s^2 (1 - 1e-6). Why that is safe: an unvisited
+ * point s has an exact minimal-image displacement t_e with |t_e| >= r_s (before
+ * the slacks). The canonical per-axis value is RN(q_d - s_d), wrapped by an exact
+ * +-L_d (R1, "periodic wrapping in the distance
+ * calculation"):
+ *   - no wrap: |RN(q-s)| >= |q-s| (1 - 2^-24)          (relative error only);
+ *   - wrap:    RN(q-s) +- L differs from q-s +- L by |RN(q-s) - (q-s)|
+ *              <= ulp(|q-s|)/2 <= 2^-24 L_d               (ABSOLUTE error: the
+ *              rounding happens before the wrap, so it is not relative to |t|).
+ * Hence |t_canon| >= |t_e| (1 - 2^-24) - sqrt(3) 2^-24 L_max, and the FP32 sum of
+ * squares loses at most another 3 * 2^-24 relative: canonical d2 >=
+ * (r_s - sqrt(3) 2^-24 L_max)^2 (1 - 6 * 2^-24) > d2_k, so no unvisited point can
+ * enter the list (not even on a tie). Also stop once every cell has been visited.
+ * (Round-1 bug: without the absolute wrap slack, cells < ~0.06 L could stop early
+ * on a wrapped pair; tests/test_oracle_knn.py::test_grid_periodic_wrap_slack.)
  */
 static void grid_query(const grid_t *g, const float *pos, const float *q, const domain_t *dom, topk_t *t) {
   int c[3];
@@ -265,6 +277,7 @@ static void grid_query(const grid_t *g, const float *pos, const float *q, const 
     if (need > smax) smax = need;
   }
   double ext = fmax(fmax(g->w[0] * g->G[0], g->w[1] * g->G[1]), g->w[2] * g->G[2]);
+  double lmax = fmax(fmax((double)dom->L[0], (double)dom->L[1]), (double)dom->L[2]);
   for (int s = 0; s <= smax; ++s) {
     /* visit the cells with Chebyshev distance exactly s (deduplicated when wrapped) */
     int lo[3], hi[3];
@@ -318,6 +331,7 @@ static void grid_query(const grid_t *g, const float *pos, const float *q, const 
     }
     if (all_covered) break;
     rs -= 1e-12 * ext;
+    if (dom->periodic) rs -= 1.7320508075688772 * 0x1p-24 * lmax;
     if (t->cnt == t->k && rs > 0 && (double)t->d[t->k - 1] < rs * rs * (1.0 - 1e-6)) break;
   }
 }
@@ -368,9 +382,14 @@ void oracle_pair_d2(const float *a, const float *b, int64_t m, const float *box,
  * higher index root to point towards the lower index root"), so every root is its
  * component's minimum.
  *   oracle_fof_brute : every pair i < j, O(N^2).
- *   oracle_fof_grid  : cells of width >= 1.0001 r_link, pairs in the 27 neighbouring
- *                      cells (a linked pair is closer than one cell width on every
- *                      axis); same labels (pinned against brute in tests).
+ *   oracle_fof_grid  : cells of width >= 1.0001 r_link (+ 2 * 2^-24 L_max when
+ *                      periodic), pairs in the 27 neighbouring cells (a linked pair
+ *                      is closer than one cell width on every axis); same labels
+ *                      (pinned against brute in tests).
+ * Why the periodic term: a linked pair has canonical |t_d| <= sqrt(b2)(1 + 2^-23),
+ * but a wrapped t_d = RN(q-s) +- L carries an absolute error up to 2^-24 L_d
+ * (the rounding precedes the exact wrap, see grid_query), so the exact
+ * per-axis separation can exceed r_link by that much.
  */
 static int32_t uf_find(int32_t *par, int32_t x) {
   while (par[x] != x) {
@@ -408,7 +427,8 @@ int oracle_fof_brute(const float *pos, int64_t n, const float *box, float b2, in
 int oracle_fof_grid(const float *pos, int64_t n, const float *box, float b2, int32_t *label) {
   domain_t dom;
   make_domain(&dom, box);
-  const double w = sqrt((double)b2) * 1.0001;
+  double w = sqrt((double)b2) * 1.0001;
+  if (dom.periodic) w += 2.0 * 0x1p-24 * fmax(fmax((double)dom.L[0], (double)dom.L[1]), (double)dom.L[2]);
   double lo[3], span[3];
   for (int d = 0; d < 3; ++d) {
     lo[d] = dom.periodic ? 0.0 : INFINITY;

@@ -63,6 +63,24 @@ def test_grid_equals_brute(kind, box):
     assert np.array_equal(fof_labels(p, r, box, "grid"), fof_labels(p, r, box, "brute"))
 
 
+def test_grid_equals_brute_across_the_wrap():
+    """Pairs linked across the periodic face at linking lengths down to the finest grid cell
+    (the canonical wrapped t = RN(q - s) +- L carries an absolute error ~ulp(L)/2, R1):
+    the grid's cell width keeps every such pair in neighbouring cells."""
+    r = np.random.default_rng(5)
+    for rl in (1e-3, 1.2e-3, 3e-3):
+        pts = []
+        for _ in range(400):
+            a = r.random(3)
+            a[0] = 1.0 - r.random() * rl
+            b = a.copy()
+            b[0] = (a[0] + rl * (0.9 + 0.2 * r.random())) % 1.0
+            pts += [a, b]
+        p = np.asarray(pts, np.float32)
+        p = np.where(p >= 1, 0, p).astype(np.float32)
+        assert np.array_equal(fof_labels(p, rl, 1.0, "grid"), fof_labels(p, rl, 1.0, "brute"))
+
+
 @pytest.mark.parametrize("box", [1.0, None])
 def test_scipy_connected_components(box):
     """Independent FP64 cross-check: same partition as cKDTree.query_pairs + csgraph (no pair is
