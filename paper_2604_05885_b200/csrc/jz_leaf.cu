@@ -51,7 +51,11 @@ static_assert(JZ_LCAP >= kMaxLeaf, "a leaf must fit the staging buffer");
 #define JZ_LOGX 16  // K = 16: 32-entry log (10 KB per one-warp CTA with staging)
 #endif
 #ifndef JZ_STATS
-#define JZ_STATS 1  // per-lane walk counters (appends, merge rounds, compactions, staged leaves)
+#define JZ_STATS 0  // per-lane walk counters (appends, merge rounds, compactions): diagnostic builds (tools/mkvar.py)
+#endif
+
+#ifndef JZ_LANE_TEST
+#define JZ_LANE_TEST 1  // per-lane point-box test of each leaf that passes the warp-box test
 #endif
 
 #ifndef JZ_LOGX32
@@ -502,7 +506,7 @@ __device__ __forceinline__ void visit_leaves(const LeafPK &a, const Dom &D, Warp
         const int src = __ffs(bal) - 1;
         if (__shfl_sync(0xffffffffu, cls, src) != c0) break;
         // per-lane test: does any lane's query reach this leaf within its own k-th value?
-        {
+        if (JZ_LANE_TEST) {
           const float lcx = __shfl_sync(0xffffffffu, cx, src), lcy = __shfl_sync(0xffffffffu, cy, src),
                       lcz = __shfl_sync(0xffffffffu, cz, src);
           const float lex = __shfl_sync(0xffffffffu, ex, src), ley = __shfl_sync(0xffffffffu, ey, src),
