@@ -95,13 +95,16 @@ def _config(name, n_override=None):
     return pos, box, k, c, time.time() - t0
 
 
-def cpu_baseline(pos, box, k, sample_rows=200_000, seed=0):
-    """The oracle (grid search, as it stands) on the host cores: grid build over the full set
-    plus a random sample of query rows; projected to the full row count."""
+def cpu_baseline(pos, box, k, sample_rows=1_000_000, seed=0):
+    """The oracle (grid search, as it stands) on the host cores over a bounded, FIXED sample of
+    the workload: the grid over all n points plus `sample_rows` query rows drawn once with a
+    fixed seed (the same rows every run, so runs repeat the same work). value = sampled rows /
+    measured time, with the grid build charged per row (t_build * rows / n): a measured
+    throughput on the sample, not a projection of the whole job's time."""
     from oracle import knn_grid, oracle_threads
 
     n = pos.shape[0]
-    rows = np.random.default_rng(seed).choice(n, min(sample_rows, n), replace=False)
+    rows = np.sort(np.random.default_rng(seed).choice(n, min(sample_rows, n), replace=False))
     t0 = time.perf_counter()
     knn_grid(pos, k, box, rows=rows[:0])
     t_build = time.perf_counter() - t0
@@ -109,11 +112,19 @@ def cpu_baseline(pos, box, k, sample_rows=200_000, seed=0):
     knn_grid(pos, k, box, rows=rows)
     t_all = time.perf_counter() - t0
     t_q = max(t_all - t_build, 1e-9)
-    t_full = t_build + t_q * n / len(rows)
-    return {"value": n / t_full, "unit": UNIT, "cores": oracle_threads(), "kind": "oracle",
-            "sample": f"oracle grid search on the C4 set: grid over all {n} points ({t_build:.2f} s) + "
-                      f"{len(rows)} random query rows ({t_q:.2f} s), projected to all {n} rows "
-                      f"({t_full:.1f} s)"}, t_full
+    t_charged = t_q + t_build * len(rows) / n
+    return {"value": len(rows) / t_charged, "unit": UNIT, "cores": oracle_threads(), "kind": "oracle",
+            "sample": f"oracle grid search on the {n}-point set: grid over all points ({t_build:.2f} s, charged "
+                      f"{len(rows)}/{n} of it) + {len(rows)} fixed random query rows (seed {seed}, {t_q:.2f} s); "
+                      f"value = rows / charged time, measured, not projected"}, t_all + t_build
+
+
+def _l2_note(n, k):
+    """Whether one step's inputs / outputs exceed the 126 MB L2 (no flush is done between steps)."""
+    pin, pout = n * 12, n * k * 8
+    big = pin + pout > 126e6
+    return (f"inputs {pin / 1e6:.3g} MB positions + {pout / 1e6:.3g} MB rows "
+            + ("exceed the 126 MB L2; no flush" if big else "fit in the 126 MB L2 (no flush; small config)"))
 
 
 def run_reference(args):
@@ -123,20 +134,22 @@ def run_reference(args):
         return
     pos, box, k, c, _ = _config(args.config, args.n)
     for _ in range(args.warmup):
-        cpu_baseline(pos, box, k, sample_rows=args.ref_rows, seed=1)
+        cpu_baseline(pos, box, k, sample_rows=args.ref_rows)
     vals, times = [], []
     cb = None
     for s in range(args.steps):
-        cb, t_full = cpu_baseline(pos, box, k, sample_rows=args.ref_rows, seed=2 + s)
+        cb, t_full = cpu_baseline(pos, box, k, sample_rows=args.ref_rows)
         vals.append(cb["value"])
         times.append(t_full)
     v = float(np.median(vals))
+    spread = [float(min(vals)), float(max(vals))]
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * float(np.median(times)), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": args.config, "n_points": int(pos.shape[0]), "k": k,
-                       "box": "periodic L=1" if box else "open", "distribution": c["kind"]},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cb["cores"], "kind": "oracle", "sample": cb["sample"]},
+                       "box": "periodic L=1" if box else "open", "distribution": c["kind"], "order": "input", "l2": _l2_note(pos.shape[0], k)},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cb["cores"], "kind": "oracle", "sample": cb["sample"],
+                             "spread": spread},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -156,8 +169,10 @@ def run_single(args):
     d2 = torch.empty((n, k), dtype=torch.float32, device=dev)
     jz.set_timing(True)
 
+    prm = {"nmax0": args.nmax0} if args.nmax0 else None
+
     def step():
-        ix = jz.KnnIndex(d_pos, box=box)
+        ix = jz.KnnIndex(d_pos, box=box, params=prm)
         ix.query(k, out=(idx, d2, None))
         t = ix.stage_times()
         ix.free()
@@ -212,7 +227,7 @@ def run_single(args):
             "data": "synthetic",
             "config": {"workload": args.config, "n_points": n, "k": k, "box": "periodic L=1" if box else "open",
                        "distribution": c["kind"], "order": "input",
-                       "l2": "inputs (1.2 GB positions, 12.8 GB outputs) exceed the 126 MB L2; no flush"},
+                       "l2": _l2_note(n, k)},
             "roofline": roofline, "stages_ms": st_ms, "dominant_stage": dominant, "evals_per_query": evals / n, "inserts_per_query": inserts / n,
             "walk_per_item": {kk: v / max(1, stages[-1]["walk"]["items"]) for kk, v in stages[-1]["walk"].items()},
             "gpu_launches": int(launches * args.steps), "clocks": clocks}
@@ -254,7 +269,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C4")
     ap.add_argument("--n", type=int, default=None, help="override the point count (tests)")
-    ap.add_argument("--ref-rows", type=int, default=200_000)
+    ap.add_argument("--nmax0", type=int, default=0, help="leaf capacity N_max^(0) override (tuning experiments)")
+    ap.add_argument("--ref-rows", type=int, default=1_000_000)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true", help="kernel-only run for ncu (no e2e / baseline / clocks)")

@@ -395,6 +395,10 @@ namespace jz {
 void set_last_error(const std::string &m) { g_err = m; }
 }  // namespace jz
 
+#ifdef JZ_SEED_EXP
+namespace jz { void exp_set_seed(const float *p); }
+extern "C" __attribute__((visibility("default"))) void jz_exp_seed(const float *p) { jz::exp_set_seed(p); }
+#endif
 extern "C" {
 
 const char *jz_last_error(void) { return g_err.c_str(); }
@@ -513,6 +517,12 @@ int jz_knn_query(jz_knn_index *ix, int k, int order, int32_t *out_idx, float *ou
   ix->evals = (long long)ev[0];
   ix->inserts = (long long)ev[1];
   for (int i = 0; i < 5; ++i) ix->walk[i] = (long long)ev[2 + i];
+  if (getenv("JZ_DIAG_STATS") && ev[6]) {  // diagnostic builds (-DJZ_STATS=1): per-item own-pass / walk split
+    const double it = (double)ev[6];
+    fprintf(stderr, "JZ_STATS per item: appends %.1f (own %.1f) rounds %.1f (own %.1f) compactions %.2f (own %.2f) "
+            "steps %.1f (own %.1f) passing %.1f (own %.1f) staged %.1f\n", ev[2] / it, ev[7] / it, ev[3] / it, ev[8] / it,
+            ev[4] / it, ev[9] / it, ev[12] / it, ev[10] / it, ev[13] / it, ev[11] / it, ev[5] / it);
+  }
 
   if (ix->timing) {
     cudaEventElapsedTime(&ix->times[3], ix->ev[4], ix->ev[5]);

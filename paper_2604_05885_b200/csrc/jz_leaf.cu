@@ -54,6 +54,10 @@ static_assert(JZ_LCAP >= kMaxLeaf, "a leaf must fit the staging buffer");
 #define JZ_STATS 0  // per-lane walk counters (appends, merge rounds, compactions): diagnostic builds (tools/mkvar.py)
 #endif
 
+#ifndef JZ_MERGE_T
+#define JZ_MERGE_T 0  // > 0: merge at a batch end only when some lane has >= JZ_MERGE_T new log entries
+#endif
+
 #ifndef JZ_LANE_TEST
 #define JZ_LANE_TEST 1  // per-lane point-box test of each leaf that passes the warp-box test
 #endif
@@ -232,6 +236,8 @@ struct Lane {
   unsigned rnd;   // merge rounds (warp-uniform)
   unsigned cmp;   // compactions (warp-uniform)
   unsigned stg;   // staged leaves (warp-uniform)
+  unsigned stp;   // 8-source eval steps (warp-uniform, JZ_STATS)
+  unsigned pst;   // steps whose vote passed (warp-uniform, JZ_STATS)
   bool act;
 };
 
@@ -385,7 +391,9 @@ __device__ __forceinline__ void eval_block(WarpBuf<K> &B, int n, float qx, float
       b3 = u + 7u < (unsigned)mw ? nan : b3;
     }
     const float m = fminf(fminf(fminf(a0, a1), fminf(a2, a3)), fminf(fminf(b0, b1), fminf(b2, b3)));  // NaN ignored
+    if (JZ_STATS) ++L.stp;
     if (__any_sync(0xffffffffu, m <= L.kth)) {
+      if (JZ_STATS) ++L.pst;
       const int4 G = *reinterpret_cast<const int4 *>(&B.g[j]);
       const int4 H = *reinterpret_cast<const int4 *>(&B.g[j + 4]);
       append<K, LB>(B, L, a0, G.x);
@@ -400,6 +408,9 @@ __device__ __forceinline__ void eval_block(WarpBuf<K> &B, int n, float qx, float
     }
   }
   // refresh the k-th value for the next pruning decisions (merge rounds = max new entries)
+#if JZ_MERGE_T > 0
+  if (__any_sync(0xffffffffu, L.nl - L.nf >= JZ_MERGE_T))
+#endif
   merge<K, LB>(B, L);
 }
 
@@ -418,6 +429,36 @@ __device__ __forceinline__ int pad8(WarpBuf<K> &B, int n) {
     n += 4;
   }
   return n;
+}
+
+// asynchronous 4-byte global -> shared copies (LDGSTS): every source of a batch is in flight at
+// once and no registers hold staged data; cp.async.wait_all + __syncwarp before the batch is read
+__device__ __forceinline__ void cpa4(void *sdst, const void *gsrc) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// stage m sources (float4 {x, y, z, bits(gidx)} at src) into slots [n, n + mp) as SoA; the
+// slots [n + m, n + mp) (mp = m rounded up to 4) get NaN coordinates
+template <int K>
+__device__ __forceinline__ void stage_async(WarpBuf<K> &B, int n, const float4 *__restrict__ src, int m, int mp) {
+  const int lane = threadIdx.x & 31;
+  for (int t = lane; t < mp; t += 32) {
+    if (t < m) {
+      const float *p = reinterpret_cast<const float *>(src + t);
+      cpa4(&B.x[n + t], p);
+      cpa4(&B.y[n + t], p + 1);
+      cpa4(&B.z[n + t], p + 2);
+      cpa4(&B.g[n + t], p + 3);
+    } else {
+      const float nan = __int_as_float(0x7fc00000);
+      B.x[n + t] = nan;
+      B.y[n + t] = nan;
+      B.z[n + t] = nan;
+      B.g[n + t] = 0;
+    }
+  }
 }
 
 template <int K, bool LB, int MW = 0>
@@ -463,14 +504,41 @@ struct LeafPK {
   unsigned long long *stats;  // counters (jz_knn_stats) or nullptr
 };
 
+// Pending batch of staged source leaves (one periodic shift class), carried across source nodes
+// so that batches are full: n staged slots, c0 their class.
+struct Batch {
+  int n;
+  int c0;
+};
+
+// evaluate the pending batch against the lane's query and refresh the k-th value
+template <int K, bool LB, bool PER>
+__device__ __forceinline__ void flush(WarpBuf<K> &B, Batch &W, float qx, float qy, float qz, const Dom &D,
+                                      Lane<K, LB> &L) {
+  if (W.n == 0) return;
+  const int n = pad8<K>(B, W.n);
+  cpa_wait();
+  __syncwarp();
+  const int c0 = W.c0;
+  if (!PER || !any_straddle(c0)) {  // no axis straddles: no wrap, or a uniform exact shift
+    eval_block<K, LB>(B, n, qx, qy, qz, PER && c0 != 0, class_shift(c0 & 3, D.L[0]), class_shift((c0 >> 2) & 3, D.L[1]),
+                      class_shift((c0 >> 4) & 3, D.L[2]), L, 0, 0);
+  } else {
+    eval_generic<K, LB>(B, n, qx, qy, qz, D, L);
+  }
+  __syncwarp();
+  W.n = 0;
+}
+
 // Visit the child leaves [la, lb) of one source node, skipping [xa, xb): one lane tests one
 // leaf against the warp's query box (bound vs the warp's current max k-th value), then every
 // lane tests its own query against each surviving leaf (skip unless some lane needs it);
-// survivors are staged in batches of one periodic shift class and evaluated.
+// survivors are appended to the pending batch (asynchronous copies), which is evaluated when
+// it is full, when the shift class changes, or at the end of the walk.
 template <int K, bool LB, bool PER>
-__device__ __forceinline__ void visit_leaves(const LeafPK &a, const Dom &D, WarpBuf<K> &B, const CE &wb, float wmax,
-                                             int la, int lb, int xa, int xb, float qx, float qy, float qz, bool act,
-                                             Lane<K, LB> &L, unsigned long long &nev) {
+__device__ __forceinline__ void visit_leaves(const LeafPK &a, const Dom &D, WarpBuf<K> &B, Batch &W, const CE &wb,
+                                             float wmax, int la, int lb, int xa, int xb, float qx, float qy, float qz,
+                                             bool act, Lane<K, LB> &L, unsigned long long &nev) {
   const int lane = threadIdx.x & 31;
   for (int l0 = la; l0 < lb; l0 += 32) {
     const int l = l0 + lane;
@@ -499,51 +567,31 @@ __device__ __forceinline__ void visit_leaves(const LeafPK &a, const Dom &D, Warp
     JZ_DIAG(2, 1);
     JZ_DIAG(3, __popc(bal));
     while (bal) {
-      // batch consecutive surviving leaves of one shift class into the warp buffer
-      const int c0 = __shfl_sync(0xffffffffu, cls, __ffs(bal) - 1);
-      int n = 0;
-      while (bal) {
-        const int src = __ffs(bal) - 1;
-        if (__shfl_sync(0xffffffffu, cls, src) != c0) break;
-        // per-lane test: does any lane's query reach this leaf within its own k-th value?
-        if (JZ_LANE_TEST) {
-          const float lcx = __shfl_sync(0xffffffffu, cx, src), lcy = __shfl_sync(0xffffffffu, cy, src),
-                      lcz = __shfl_sync(0xffffffffu, cz, src);
-          const float lex = __shfl_sync(0xffffffffu, ex, src), ley = __shfl_sync(0xffffffffu, ey, src),
-                      lez = __shfl_sync(0xffffffffu, ez, src);
-          const float dl = dlow2_ce<PER>(__fsub_rn(qx, lcx), __fsub_rn(qy, lcy), __fsub_rn(qz, lcz), lex, ley, lez, D);
-          if (!__any_sync(0xffffffffu, dl <= L.kth)) {
-            bal &= bal - 1;
-            continue;
-          }
-        }
-        const int lp = __shfl_sync(0xffffffffu, s0, src), m = __shfl_sync(0xffffffffu, s1, src) - lp;
-        if (n + ((m + 3) & ~3) > kLCap) break;
-        bal &= bal - 1;
-        for (int t = lane; t < ((m + 3) & ~3); t += 32) {
-          float4 p = make_float4(__int_as_float(0x7fc00000), __int_as_float(0x7fc00000), __int_as_float(0x7fc00000),
-                                 0.f);
-          if (t < m) p = a.spts[lp + t];
-          B.x[n + t] = p.x;
-          B.y[n + t] = p.y;
-          B.z[n + t] = p.z;
-          B.g[n + t] = __float_as_int(p.w);
-        }
-        nev += act ? (unsigned)m : 0u;
-        JZ_DIAG(4, 1);
-        ++L.stg;
-        n += (m + 3) & ~3;
+      const int src = __ffs(bal) - 1;
+      bal &= bal - 1;
+      // per-lane test: does any lane's query reach this leaf within its own k-th value?
+      if (JZ_LANE_TEST) {
+        const float lcx = __shfl_sync(0xffffffffu, cx, src), lcy = __shfl_sync(0xffffffffu, cy, src),
+                    lcz = __shfl_sync(0xffffffffu, cz, src);
+        const float lex = __shfl_sync(0xffffffffu, ex, src), ley = __shfl_sync(0xffffffffu, ey, src),
+                    lez = __shfl_sync(0xffffffffu, ez, src);
+        const float dl = dlow2_ce<PER>(__fsub_rn(qx, lcx), __fsub_rn(qy, lcy), __fsub_rn(qz, lcz), lex, ley, lez, D);
+        if (!__any_sync(0xffffffffu, dl <= L.kth)) continue;
+        JZ_DIAG(6, (unsigned long long)__popc(__ballot_sync(0xffffffffu, act && dl <= L.kth)) *
+                       (unsigned)(__shfl_sync(0xffffffffu, s1, src) - __shfl_sync(0xffffffffu, s0, src)));
+        JZ_DIAG(7, (unsigned long long)__popc(__ballot_sync(0xffffffffu, act)) *
+                       (unsigned)(__shfl_sync(0xffffffffu, s1, src) - __shfl_sync(0xffffffffu, s0, src)));
       }
-      if (n == 0) continue;
-      n = pad8<K>(B, n);
-      __syncwarp();
-      if (!PER || !any_straddle(c0)) {  // no axis straddles: no wrap, or a uniform exact shift
-        eval_block<K, LB>(B, n, qx, qy, qz, PER && c0 != 0, class_shift(c0 & 3, D.L[0]),
-                          class_shift((c0 >> 2) & 3, D.L[1]), class_shift((c0 >> 4) & 3, D.L[2]), L, 0, 0);
-      } else {
-        eval_generic<K, LB>(B, n, qx, qy, qz, D, L);
-      }
-      __syncwarp();
+      const int c = __shfl_sync(0xffffffffu, cls, src);
+      const int lp = __shfl_sync(0xffffffffu, s0, src), m = __shfl_sync(0xffffffffu, s1, src) - lp;
+      const int mp = (m + 3) & ~3;
+      if (W.n > 0 && (c != W.c0 || W.n + mp > kLCap)) flush<K, LB, PER>(B, W, qx, qy, qz, D, L);
+      if (W.n == 0) W.c0 = c;
+      stage_async<K>(B, W.n, a.spts + lp, m, mp);
+      W.n += mp;
+      nev += act ? (unsigned)m : 0u;
+      JZ_DIAG(4, 1);
+      ++L.stg;
     }
   }
 }
@@ -639,16 +687,10 @@ __device__ __forceinline__ void own_pass(const LeafPK &a, const Dom &D, WarpBuf<
   const int lane = threadIdx.x & 31;
   for (int b0 = s0; b0 < s1; b0 += kLCap) {
     const int m = min(kLCap, s1 - b0), mp = (m + 3) & ~3;
-    for (int t = lane; t < mp; t += 32) {
-      float4 p = make_float4(__int_as_float(0x7fc00000), __int_as_float(0x7fc00000), __int_as_float(0x7fc00000), 0.f);
-      if (t < m) p = a.spts[b0 + t];
-      B.x[t] = p.x;
-      B.y[t] = p.y;
-      B.z[t] = p.z;
-      B.g[t] = __float_as_int(p.w);
-    }
+    stage_async<K>(B, 0, a.spts + b0, m, mp);
     nev += act ? (unsigned)m : 0u;
     const int np = pad8<K>(B, mp);
+    cpa_wait();
     __syncwarp();
     const int wl = wpos - b0;
     if (!PER || cls_all == 0) {
@@ -659,6 +701,12 @@ __device__ __forceinline__ void own_pass(const LeafPK &a, const Dom &D, WarpBuf<
     __syncwarp();
   }
 }
+
+#ifdef JZ_SEED_EXP
+// experiment only (tools/mkvar.py -DJZ_SEED_EXP): per-row k-th d2 seed (ideal-threshold bound)
+__device__ const float *g_seed = nullptr;
+void exp_set_seed(const float *p) { cudaMemcpyToSymbol(g_seed, &p, sizeof(p)); }
+#endif
 
 template <int K, bool LB, bool PER>
 __global__ void __launch_bounds__(kLThreads, MinBlocks<K>::v) k_leaf(LeafPK a, Dom D) {
@@ -707,7 +755,7 @@ __global__ void __launch_bounds__(kLThreads, MinBlocks<K>::v) k_leaf(LeafPK a, D
       L.lb = ((u64)__float_as_uint(a.out_d2[o]) << 32) | (unsigned)(a.out_idx[o] + 1);
     }
     L.ins = 0;
-    L.app = L.rnd = L.cmp = L.stg = 0;
+    L.app = L.rnd = L.cmp = L.stg = L.stp = L.pst = 0;
     L.nl = 0;
     L.nf = 0;
     L.act = act;
@@ -743,10 +791,23 @@ __global__ void __launch_bounds__(kLThreads, MinBlocks<K>::v) k_leaf(LeafPK a, D
       }
       cls_all = __reduce_or_sync(0xffffffffu, cls_all);
     }
+#ifdef JZ_SEED_EXP
+    if (g_seed) {
+      const float t = act ? g_seed[row] : R0;
+#pragma unroll
+      for (int j = 0; j < K; ++j) L.F[j] = fminf(L.F[j], t);
+      L.kth = act ? L.F[K - 1] : -1.f;
+    }
+#endif
     L.stg += xb - xa;
     own_pass<K, LB, PER>(a, D, B, s0o, s1o, cls_all, wpos, qx, qy, qz, act, L, nev);
+    if (JZ_MERGE_T > 0) merge<K, LB>(B, L);
   }
+  const unsigned o_app = L.app, o_rnd = L.rnd, o_cmp = L.cmp, o_stp = L.stp, o_pst = L.pst;
   const int64_t eb = a.ispl[J], ee = a.ispl[J + 1];
+  Batch W;
+  W.n = 0;
+  W.c0 = 0;
   // entries in chunks of 32, one lane per entry (list order = r_low order): the node tests run in
   // parallel instead of one dependent load chain per entry; survivors are visited in list order
   for (int64_t c0 = eb; c0 < ee; c0 += 32) {
@@ -774,11 +835,12 @@ __global__ void __launch_bounds__(kLThreads, MinBlocks<K>::v) k_leaf(LeafPK a, D
       bal &= bal - 1;
       const int Se = __shfl_sync(0xffffffffu, S, src);
       const float wmax = a.early ? warp_max_kth(L.kth) : INFINITY;
-      visit_leaves<K, LB, PER>(a, D, B, wb, wmax, a.par_leaf[Se], a.par_leaf[Se + 1], Se == J ? xa : 0,
+      visit_leaves<K, LB, PER>(a, D, B, W, wb, wmax, a.par_leaf[Se], a.par_leaf[Se + 1], Se == J ? xa : 0,
                                Se == J ? xb : 0, qx, qy, qz, act, L, nev);
     }
     if (stop) break;
   }
+  flush<K, LB, PER>(B, W, qx, qy, qz, D, L);
   JZ_DIAG(5, 1);
   // the row: the k smallest keys of the log (all entries <= the final k-th value)
   compact<K, LB>(B, L);
@@ -799,6 +861,20 @@ __global__ void __launch_bounds__(kLThreads, MinBlocks<K>::v) k_leaf(LeafPK a, D
       atomicAdd(&a.stats[4], (unsigned long long)L.cmp);
       atomicAdd(&a.stats[5], (unsigned long long)L.stg);
       atomicAdd(&a.stats[6], 1ull);
+    }
+    if (JZ_STATS) {
+      unsigned long long oa = o_app;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) oa += __shfl_xor_sync(0xffffffffu, oa, o);
+      if (lane == 0) {
+        atomicAdd(&a.stats[7], oa);
+        atomicAdd(&a.stats[8], (unsigned long long)o_rnd);
+        atomicAdd(&a.stats[9], (unsigned long long)o_cmp);
+        atomicAdd(&a.stats[10], (unsigned long long)o_stp);
+        atomicAdd(&a.stats[11], (unsigned long long)o_pst);
+        atomicAdd(&a.stats[12], (unsigned long long)L.stp);
+        atomicAdd(&a.stats[13], (unsigned long long)L.pst);
+      }
     }
   }
   if (act) {
@@ -1203,8 +1279,9 @@ void leaf_to_leaf(const LeafArgs &a, const Dom &D, cudaStream_t st) {
     JZ_CUDA(cudaMemcpyFromSymbolAsync(h, g_diag, sizeof(h), 0, cudaMemcpyDeviceToHost, st));
     JZ_CUDA(cudaStreamSynchronize(st));
     const double it = h[5] ? (double)h[5] : 1.0;
-    fprintf(stderr, "JZ_DIAG per item: entries %.1f passing %.1f chunks %.1f leaves_warp %.1f staged %.1f (items %llu)\n",
-            h[0] / it, h[1] / it, h[2] / it, h[3] / it, h[4] / it, h[5]);
+    fprintf(stderr, "JZ_DIAG per item: entries %.1f passing %.1f chunks %.1f leaves_warp %.1f staged %.1f (items %llu) "
+            "walk pair-evals needed %.1f of %.1f\n",
+            h[0] / it, h[1] / it, h[2] / it, h[3] / it, h[4] / it, h[5], h[6] / it, h[7] / it);
     const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     JZ_CUDA(cudaMemcpyToSymbolAsync(g_diag, z, sizeof(z), 0, cudaMemcpyHostToDevice, st));
   }
