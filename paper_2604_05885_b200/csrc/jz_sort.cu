@@ -10,6 +10,7 @@
 // memory in digit order, and writes contiguous runs. Pass 0 computes keys from positions
 // (no key/val read); the last pass gathers float4 {x, y, z, bits(gidx)} (no separate
 // gather kernel). Passes whose digit is constant over all keys are skipped.
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -250,6 +251,306 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_onesweep(
   }
 }
 
+// ---------------------------------------------------------------- A3 (default): 40-bit key sort, 8-byte items
+// The LSD passes sort key bits 23..62 (the 40 most significant of the 63 key bits) with 8-byte
+// (key part, index) items instead of 12-byte (key, index) pairs, five 8-bit passes instead of
+// eight: pass 0 ranks bits 23..30, computed from the positions; passes 1-4 rank hi = key >> 31.
+// The last pass gathers the positions, recomputes the full 63-bit keys and writes keys +
+// float4 points + perm. Points whose bits 23..62 agree (cells of 2^-13.3 of the box side: rare
+// even at halo centres) are then in input order; a fix-up orders each such run by (key, index),
+// which makes the result the stable argsort of the full keys. Runs longer than
+// kSegBlock (massive duplicates) fall back to the 8-pass sort of the full keys.
+constexpr int kS32Threads = 256;
+constexpr int kS32IPT = 16;
+constexpr int kS32Tile = kS32Threads * kS32IPT;
+constexpr int kS32Passes = 5;     // pass 0: key bits 23..30; passes 1-4: the bytes of hi = key >> 31
+constexpr int kLoShift = 23;
+constexpr int kSegThread = 32;    // runs up to this length: one thread, insertion sort in place
+constexpr int kSegBlock = 2048;   // runs up to this length: one CTA, bitonic sort in shared memory
+
+__device__ __forceinline__ uint32_t hi32(uint64_t k) { return (uint32_t)(k >> 31); }
+__device__ __forceinline__ uint64_t runkey(uint64_t k) { return k >> kLoShift; }  // equal => fix-up run
+
+__global__ void __launch_bounds__(256) k_hist32(const float *__restrict__ pos, int64_t n, int stride, Frame f,
+                                                unsigned int *__restrict__ hist /*[4][256]*/) {
+  __shared__ unsigned int s_h[kS32Passes][kRadix];
+  for (int i = threadIdx.x; i < kS32Passes * kRadix; i += blockDim.x) (&s_h[0][0])[i] = 0;
+  __syncthreads();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float *p = pos + i * stride;
+    const uint64_t k = morton(p[0], p[1], p[2], f);
+    const uint32_t h = hi32(k);
+    atomicAdd(&s_h[0][(k >> kLoShift) & 255], 1u);
+#pragma unroll
+    for (int ps = 1; ps < kS32Passes; ++ps) atomicAdd(&s_h[ps][(h >> (8 * (ps - 1))) & 255], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kS32Passes * kRadix; i += blockDim.x) {
+    const unsigned v = (&s_h[0][0])[i];
+    if (v) atomicAdd(&hist[i], v);
+  }
+}
+
+__device__ __forceinline__ void cpa16(void *sdst, const void *gsrc) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gsrc) : "memory");
+}
+
+// input point v as float4 {x, y, z, bits(gidx)} (gidx_mode: input rows are float4 {x, y, z, gidx})
+__device__ __forceinline__ float4 load_point(const float *__restrict__ pos, int stride, int gidx_mode, int64_t gidx_base,
+                                             uint32_t v) {
+  if (gidx_mode) return reinterpret_cast<const float4 *>(pos)[v];
+  const float *p = pos + (int64_t)v * stride;
+  return make_float4(p[0], p[1], p[2], __int_as_float((int)(gidx_base + v)));
+}
+
+// One-sweep pass over (hi, index) pairs. Non-first passes bring the tile into shared memory with
+// 16-byte asynchronous copies (every load of the tile in flight at once), then rank as above.
+template <bool FIRST, bool LAST>
+__global__ void __launch_bounds__(kS32Threads, 3) k_onesweep32(
+    const float *__restrict__ pos, int stride, int gidx_mode, int64_t gidx_base, Frame f,
+    const uint32_t *__restrict__ kin, const uint32_t *__restrict__ vin, uint32_t *__restrict__ kout,
+    uint32_t *__restrict__ vout, uint64_t *__restrict__ keys_out, float4 *__restrict__ pts_out, int64_t n, int shift,
+    int lo, const unsigned int *__restrict__ digit_base, unsigned long long *status, int *tile_counter) {
+  // FIRST && lo: the item key is (key >> 23) mod 2^32 (digit = bits 23..30, shift 0) and the hi
+  // part written for the next pass is recomputed from the position; otherwise items carry hi
+  __shared__ unsigned int s_wcnt[kS32Threads / 32][kRadix];
+  __shared__ __align__(16) uint32_t s_keys[kS32Tile];
+  __shared__ __align__(16) uint32_t s_vals[kS32Tile];
+  __shared__ unsigned int s_tstart[kRadix];
+  __shared__ unsigned long long s_gbase[kRadix];
+  __shared__ unsigned s_ws[kS32Threads / 32];
+  __shared__ int s_tile;
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < (kS32Threads / 32) * kRadix; i += kS32Threads) (&s_wcnt[0][0])[i] = 0;
+  if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1);
+  __syncthreads();
+  const int tile = s_tile;
+  const int64_t base = (int64_t)tile * kS32Tile;
+  const int cnt = (int)min((int64_t)kS32Tile, n - base);
+
+  uint32_t key[kS32IPT], val[kS32IPT], rank[kS32IPT];
+  if (!FIRST) {
+    if (cnt == kS32Tile) {  // full tile: 16-byte copies of keys and values
+#pragma unroll
+      for (int c = threadIdx.x; c < kS32Tile / 4; c += kS32Threads) {
+        cpa16(&s_keys[4 * c], kin + base + 4 * c);
+        cpa16(&s_vals[4 * c], vin + base + 4 * c);
+      }
+      asm volatile("cp.async.wait_all;" ::: "memory");
+    } else {
+      for (int j = threadIdx.x; j < cnt; j += kS32Threads) {
+        s_keys[j] = kin[base + j];
+        s_vals[j] = vin[base + j];
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < kS32IPT; ++i) {
+    const int j = warp * 32 * kS32IPT + i * 32 + lane;  // warp-striped: stable ranking order
+    if (j < cnt) {
+      if (FIRST) {
+        const float *p = pos + (base + j) * stride;
+        const uint64_t k64 = morton(p[0], p[1], p[2], f);
+        key[i] = lo ? (uint32_t)(k64 >> kLoShift) : hi32(k64);
+        val[i] = (uint32_t)(base + j);
+      } else {
+        key[i] = s_keys[j];
+        val[i] = s_vals[j];
+      }
+    } else {
+      key[i] = 0xffffffffu;
+      val[i] = 0;
+    }
+  }
+  if (!FIRST) __syncthreads();  // s_keys / s_vals are reused for the digit-ordered tile below
+  const unsigned lt_mask = (1u << lane) - 1u;
+#pragma unroll
+  for (int i = 0; i < kS32IPT; ++i) {
+    const int j = warp * 32 * kS32IPT + i * 32 + lane;
+    const unsigned d = j < cnt ? (key[i] >> shift) & 255u : 256u;
+    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    const unsigned before = d < 256 ? s_wcnt[warp][d] : 0u;
+    rank[i] = before + __popc(peers & lt_mask);
+    __syncwarp();
+    if (d < 256 && lane == 31 - __clz(peers)) s_wcnt[warp][d] = before + __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  const int t = threadIdx.x;
+  unsigned tot = 0;
+#pragma unroll
+  for (int w = 0; w < kS32Threads / 32; ++w) {
+    const unsigned c = s_wcnt[w][t];
+    s_wcnt[w][t] = tot;
+    tot += c;
+  }
+  unsigned long long *my_status = status + (size_t)tile * kRadix + t;
+  st_relaxed(my_status, (tile == 0 ? kFlagPre : kFlagAgg) | (unsigned long long)tot);
+  {
+    unsigned v = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned u = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += u;
+    }
+    if (lane == 31) s_ws[warp] = v;
+    __syncthreads();
+    unsigned wpre = 0;
+#pragma unroll
+    for (int w = 0; w < kS32Threads / 32; ++w) wpre += (w < warp) ? s_ws[w] : 0u;
+    s_tstart[t] = wpre + v - tot;
+  }
+  unsigned long long excl = 0;
+  if (tile > 0) {
+    int jt = tile - 1;
+    while (true) {
+      const unsigned long long sv = ld_relaxed(status + (size_t)jt * kRadix + t);
+      const unsigned long long flag = sv & ~kValMask;
+      if (flag == 0) continue;
+      excl += sv & kValMask;
+      if (flag == kFlagPre) break;
+      --jt;
+    }
+    st_relaxed(my_status, kFlagPre | (excl + tot));
+  }
+  s_gbase[t] = (unsigned long long)digit_base[t] + excl;
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < kS32IPT; ++i) {
+    const int j = warp * 32 * kS32IPT + i * 32 + lane;
+    if (j < cnt) {
+      const unsigned d = (key[i] >> shift) & 255u;
+      const unsigned lp = s_tstart[d] + s_wcnt[warp][d] + rank[i];
+      s_keys[lp] = key[i];
+      s_vals[lp] = val[i];
+    }
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < cnt; j += kS32Threads) {
+    const uint32_t k = s_keys[j];
+    const uint32_t v = s_vals[j];
+    const unsigned d = (k >> shift) & 255u;
+    const int64_t gp = (int64_t)s_gbase[d] + (j - (int)s_tstart[d]);
+    if (LAST) {
+      vout[gp] = v;  // perm
+      const float4 p = load_point(pos, stride, gidx_mode, gidx_base, v);
+      keys_out[gp] = morton(p.x, p.y, p.z, f);
+      pts_out[gp] = p;
+    } else {
+      if (FIRST && lo) {  // the tile's points were just read: the position is in L1 / L2
+        const float *p = pos + (int64_t)v * stride;
+        kout[gp] = hi32(morton(p[0], p[1], p[2], f));
+      } else {
+        kout[gp] = k;
+      }
+      vout[gp] = v;
+    }
+  }
+}
+
+__device__ __forceinline__ bool key_less(uint64_t ka, uint32_t pa, uint64_t kb, uint32_t pb) {
+  return ka < kb || (ka == kb && pa < pb);
+}
+
+// Fix-up of runs of equal hi parts (in input order after the passes): every run of length >= 2
+// is sorted by (key, index). Runs up to kSegThread: the thread at the run start, insertion sort
+// in place (key, perm and point move together); longer runs are queued for k_seg_block.
+__global__ void k_seg_fix(uint64_t *__restrict__ keys, int32_t *__restrict__ perm, float4 *__restrict__ pts, int64_t n,
+                          int64_t *__restrict__ big, int *__restrict__ nbig, int big_cap, int *__restrict__ fallback) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i + 1 < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t h = runkey(keys[i]);
+    if (runkey(keys[i + 1]) != h) continue;
+    if (i > 0 && runkey(keys[i - 1]) == h) continue;  // not the run start
+    int64_t e = i + 2;
+    while (e < n && e - i <= kSegThread && runkey(keys[e]) == h) ++e;
+    const int64_t len = e - i;
+    if (len > kSegThread) {
+      const int b = atomicAdd(nbig, 1);
+      if (b < big_cap) big[b] = i;
+      else atomicOr(fallback, 1);
+      continue;
+    }
+    for (int64_t a = i + 1; a < e; ++a) {  // insertion sort by (key, index)
+      const uint64_t ka = keys[a];
+      const int32_t pa = perm[a];
+      const float4 qa = pts[a];
+      int64_t b = a - 1;
+      while (b >= i && key_less(ka, (uint32_t)pa, keys[b], (uint32_t)perm[b])) {
+        keys[b + 1] = keys[b];
+        perm[b + 1] = perm[b];
+        pts[b + 1] = pts[b];
+        --b;
+      }
+      keys[b + 1] = ka;
+      perm[b + 1] = pa;
+      pts[b + 1] = qa;
+    }
+  }
+}
+
+// one CTA per queued long run: bitonic sort of (key, index) pairs in shared memory, then the
+// points are re-gathered from the input by the sorted indices
+__global__ void __launch_bounds__(512) k_seg_block(uint64_t *__restrict__ keys, int32_t *__restrict__ perm,
+                                                   float4 *__restrict__ pts, int64_t n, const int64_t *__restrict__ big,
+                                                   const int *__restrict__ nbig, int big_cap, const float *__restrict__ pos,
+                                                   int stride, int gidx_mode, int64_t gidx_base,
+                                                   int *__restrict__ fallback) {
+  __shared__ uint64_t s_k[kSegBlock];
+  __shared__ uint32_t s_p[kSegBlock];
+  __shared__ int s_len;
+  const int nb = min(*nbig, big_cap);
+  for (int b = blockIdx.x; b < nb; b += gridDim.x) {
+    const int64_t i0 = big[b];
+    if (threadIdx.x == 0) {
+      const uint64_t h = runkey(keys[i0]);
+      int64_t e = i0 + 1;
+      while (e < n && e - i0 <= kSegBlock && runkey(keys[e]) == h) ++e;
+      s_len = (int)(e - i0);
+      if (e - i0 > kSegBlock) atomicOr(fallback, 1);
+    }
+    __syncthreads();
+    const int len = s_len;
+    if (len <= kSegBlock) {
+      int P = 1;
+      while (P < len) P <<= 1;
+      for (int j = threadIdx.x; j < P; j += blockDim.x) {
+        s_k[j] = j < len ? keys[i0 + j] : ~0ull;
+        s_p[j] = j < len ? (uint32_t)perm[i0 + j] : 0xffffffffu;
+      }
+      __syncthreads();
+      for (int size = 2; size <= P; size <<= 1) {
+        for (int stride2 = size >> 1; stride2 > 0; stride2 >>= 1) {
+          for (int j = threadIdx.x; j < P; j += blockDim.x) {
+            const int o = j ^ stride2;
+            if (o > j) {
+              const bool asc = (j & size) == 0;
+              const bool gt = key_less(s_k[o], s_p[o], s_k[j], s_p[j]);
+              if (gt == asc) {
+                const uint64_t tk = s_k[j];
+                s_k[j] = s_k[o];
+                s_k[o] = tk;
+                const uint32_t tp = s_p[j];
+                s_p[j] = s_p[o];
+                s_p[o] = tp;
+              }
+            }
+          }
+          __syncthreads();
+        }
+      }
+      for (int j = threadIdx.x; j < len; j += blockDim.x) {
+        keys[i0 + j] = s_k[j];
+        perm[i0 + j] = (int32_t)s_p[j];
+        pts[i0 + j] = load_point(pos, stride, gidx_mode, gidx_base, s_p[j]);
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // ---------------------------------------------------------------- host driver
 void compute_frame(const float *pos, int64_t n, int stride, const Dom &D, const jz_knn_params_t &prm,
                    Frame *frame, cudaStream_t st) {
@@ -301,8 +602,9 @@ void compute_frame(const float *pos, int64_t n, int stride, const Dom &D, const 
   }
 }
 
-void sort_points(const float *pos, int64_t n, int stride, int gidx_mode, int64_t gidx_base, const Frame &frame,
-                 uint64_t *keys_out, int32_t *perm_out, float4 *pts_out, cudaStream_t st) {
+// 8-pass sort of the full 63-bit keys (fallback for runs of equal high keys > kSegBlock)
+static void sort_points8(const float *pos, int64_t n, int stride, int gidx_mode, int64_t gidx_base, const Frame &frame,
+                         uint64_t *keys_out, int32_t *perm_out, float4 *pts_out, cudaStream_t st) {
   unsigned int *dhist = nullptr;
   JZ_CUDA(cudaMallocAsync(&dhist, kPasses * kRadix * sizeof(unsigned), st));
   JZ_CUDA(cudaMemsetAsync(dhist, 0, kPasses * kRadix * sizeof(unsigned), st));
@@ -372,6 +674,94 @@ void sort_points(const float *pos, int64_t n, int stride, int gidx_mode, int64_t
   if (kbuf[1]) JZ_CUDA(cudaFreeAsync(kbuf[1], st));
   if (vbuf[1]) JZ_CUDA(cudaFreeAsync(vbuf[1], st));
   JZ_CUDA(cudaFreeAsync(dhist, st));
+}
+
+static bool g_force8 = getenv("JZ_SORT8") != nullptr;  // diagnostics: always the 8-pass sort
+
+void sort_points(const float *pos, int64_t n, int stride, int gidx_mode, int64_t gidx_base, const Frame &frame,
+                 uint64_t *keys_out, int32_t *perm_out, float4 *pts_out, cudaStream_t st) {
+  if (g_force8) {
+    sort_points8(pos, n, stride, gidx_mode, gidx_base, frame, keys_out, perm_out, pts_out, st);
+    return;
+  }
+  // scratch: histograms [4][256], fix-up counters {nbig, fallback}, big-run queue
+  constexpr int kBigCap = 1 << 16;
+  unsigned int *dhist = nullptr;
+  int *dcnt = nullptr;
+  int64_t *big = nullptr;
+  JZ_CUDA(cudaMallocAsync(&dhist, kS32Passes * kRadix * sizeof(unsigned), st));
+  JZ_CUDA(cudaMemsetAsync(dhist, 0, kS32Passes * kRadix * sizeof(unsigned), st));
+  k_hist32<<<grid_for(n, 256, 148 * 4), 256, 0, st>>>(pos, n, stride, frame, dhist);
+  JZ_LAUNCH_CHECK();
+  std::vector<unsigned> hist(kS32Passes * kRadix);
+  JZ_CUDA(cudaMemcpyAsync(hist.data(), dhist, hist.size() * sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+  JZ_CUDA(cudaStreamSynchronize(st));
+  std::vector<unsigned> bases(kS32Passes * kRadix);
+  std::vector<int> passes;
+  for (int p = 0; p < kS32Passes; ++p) {
+    unsigned acc = 0;
+    bool trivial = false;
+    for (int b = 0; b < kRadix; ++b) {
+      bases[p * kRadix + b] = acc;
+      if (hist[p * kRadix + b] == (unsigned)n) trivial = true;
+      acc += hist[p * kRadix + b];
+    }
+    if (!trivial) passes.push_back(p);
+  }
+  if (passes.empty()) passes.push_back(0);
+  JZ_CUDA(cudaMemcpyAsync(dhist, bases.data(), bases.size() * sizeof(unsigned), cudaMemcpyHostToDevice, st));
+  const int64_t ntiles = ceil_div(n, kS32Tile);
+  unsigned long long *status = nullptr;
+  int *counters = nullptr;
+  uint32_t *kbuf[2] = {nullptr, nullptr}, *vbuf[2] = {nullptr, nullptr};
+  const int np = (int)passes.size();
+  JZ_CUDA(cudaMallocAsync(&status, (size_t)ntiles * kRadix * sizeof(unsigned long long), st));
+  JZ_CUDA(cudaMallocAsync(&counters, (kS32Passes + 2) * sizeof(int), st));
+  JZ_CUDA(cudaMemsetAsync(counters, 0, (kS32Passes + 2) * sizeof(int), st));
+  for (int b = 0; b < (np > 2 ? 2 : np - 1); ++b) {
+    JZ_CUDA(cudaMallocAsync(&kbuf[b], n * sizeof(uint32_t), st));
+    JZ_CUDA(cudaMallocAsync(&vbuf[b], n * sizeof(uint32_t), st));
+  }
+  for (int i = 0; i < np; ++i) {
+    const int p = passes[i];
+    const bool first = i == 0, last = i == np - 1;
+    JZ_CUDA(cudaMemsetAsync(status, 0, (size_t)ntiles * kRadix * sizeof(unsigned long long), st));
+    const uint32_t *ki = first ? nullptr : kbuf[(i - 1) & 1];
+    const uint32_t *vi = first ? nullptr : vbuf[(i - 1) & 1];
+    uint32_t *ko = last ? nullptr : kbuf[i & 1];
+    uint32_t *vo = last ? (uint32_t *)perm_out : vbuf[i & 1];
+#define JZ_PASS32(F, L)                                                                                            \
+  k_onesweep32<F, L><<<(unsigned)ntiles, kS32Threads, 0, st>>>(pos, stride, gidx_mode, gidx_base, frame, ki, vi, ko, vo, \
+                                                             keys_out, pts_out, n, p == 0 ? 0 : 8 * (p - 1),      \
+                                                             p == 0, dhist + p * kRadix, status, counters + i)
+    if (first && last) JZ_PASS32(true, true);
+    else if (first) JZ_PASS32(true, false);
+    else if (last) JZ_PASS32(false, true);
+    else JZ_PASS32(false, false);
+#undef JZ_PASS32
+    JZ_LAUNCH_CHECK();
+  }
+  // fix-up of runs of equal high keys
+  JZ_CUDA(cudaMallocAsync(&big, kBigCap * sizeof(int64_t), st));
+  int *nbig = counters + kS32Passes, *fallback = counters + kS32Passes + 1;
+  k_seg_fix<<<grid_for(n, 256, 148 * 8), 256, 0, st>>>(keys_out, perm_out, pts_out, n, big, nbig, kBigCap, fallback);
+  JZ_LAUNCH_CHECK();
+  k_seg_block<<<148 * 2, 512, 0, st>>>(keys_out, perm_out, pts_out, n, big, nbig, kBigCap, pos, stride, gidx_mode,
+                                       gidx_base, fallback);
+  JZ_LAUNCH_CHECK();
+  int fb = 0;
+  JZ_CUDA(cudaMemcpyAsync(&fb, fallback, sizeof(int), cudaMemcpyDeviceToHost, st));
+  JZ_CUDA(cudaFreeAsync(status, st));
+  JZ_CUDA(cudaFreeAsync(counters, st));
+  JZ_CUDA(cudaFreeAsync(big, st));
+  for (int b = 0; b < 2; ++b) {
+    if (kbuf[b]) JZ_CUDA(cudaFreeAsync(kbuf[b], st));
+    if (vbuf[b]) JZ_CUDA(cudaFreeAsync(vbuf[b], st));
+  }
+  JZ_CUDA(cudaFreeAsync(dhist, st));
+  JZ_CUDA(cudaStreamSynchronize(st));
+  // a run of > kSegBlock equal high keys (heavy duplicates): redo with the full-key passes
+  if (fb) sort_points8(pos, n, stride, gidx_mode, gidx_base, frame, keys_out, perm_out, pts_out, st);
 }
 
 // Morton keys only (multi-GPU splitter step)

@@ -201,6 +201,47 @@ def test_stage_keys_and_sort():
         ix.free()
 
 
+@pytest.mark.parametrize("case", ["short_runs", "cta_runs", "fallback", "near_ties"])
+def test_sort_fixup_paths(case):
+    """A3 fix-up (DESIGN.md sort): points agreeing in key bits 23..62 are ordered by (key, index)
+    by the run fix-up -- in place (runs <= 32), by one CTA (runs <= 2048), or by the 8-pass
+    full-key sort (longer runs). Every path must give the stable argsort of the full keys."""
+    jz = _jz()
+    rng = np.random.default_rng(77)
+    base = uniform_points(3000, 21, 1.0)
+    if case == "short_runs":  # many runs of 2-6 points inside one 2^-13 cell, distinct low bits
+        c = base[rng.integers(0, 3000, 4000)]
+        jit = rng.integers(0, 64, (4000, 3)).astype(np.float32) * np.float32(2.0 ** -21)
+        pos = np.concatenate([base, (c + jit) % np.float32(1.0)]).astype(np.float32)
+    elif case == "cta_runs":  # runs of 40-1500 points in single cells
+        parts = [base]
+        for m in (40, 300, 1500):
+            c = base[rng.integers(0, 3000)]
+            jit = rng.integers(0, 256, (m, 3)).astype(np.float32) * np.float32(2.0 ** -21)
+            parts.append(((c + jit) % np.float32(1.0)).astype(np.float32))
+        pos = np.concatenate(parts)
+    elif case == "fallback":  # a run of 3000 identical points: the 8-pass sort
+        pos = np.concatenate([base, np.repeat(base[:1], 3000, axis=0)])
+    else:  # keys differing only below bit 23 next to exact duplicates
+        c = np.repeat(base[:50], 8, axis=0)
+        jit = (np.arange(400) % 8)[:, None].astype(np.float32) * np.float32(2.0 ** -21)
+        pos = np.concatenate([base, (c + jit) % np.float32(1.0), c]).astype(np.float32)
+    pos = rng.permutation(pos).astype(np.float32)
+    ix = jz.KnnIndex(torch.from_numpy(pos).cuda(), box=1.0)
+    o, s = T.key_frame(pos, 1.0)
+    want = T.morton_keys(T.quantize(pos, o, s, is_scale=True))
+    order = np.argsort(want, kind="stable")
+    assert np.array_equal(ix.perm(), order)
+    assert np.array_equal(ix.sorted_keys(), want[order])
+    sp = ix.sorted_points()
+    assert np.array_equal(sp[:, :3], pos[order])
+    assert np.array_equal(sp[:, 3].view(np.int32), order.astype(np.int32))
+    idx, d2 = ix.query(8)
+    io, do = knn_brute(pos, 8, 1.0)
+    assert np.array_equal(idx.cpu().numpy(), io) and np.array_equal(d2.cpu().numpy().view(np.int32), do.view(np.int32))
+    ix.free()
+
+
 @pytest.mark.parametrize("kind", ["uniform", "clustered", "dups"])
 def test_stage_planes_vs_oracle_tree(kind):
     """A4-A7: leaf splits and every coarser plane equal the oracle's hierarchy built by the
