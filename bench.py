@@ -261,6 +261,107 @@ def run_e2e(args, pos, box, k):
             "ms_per_step": dt * 1e3, "api": "jz_knn_search_host (pinned host buffers)"}
 
 
+def run_distributed(args):
+    """N > 1 under torchrun (or --dist at N = 1): the C4 set (10^8 clustered, k = 16) split into
+    contiguous input slices, one per rank; jz_knn_build_dist + jz_knn_query_dist on an NCCL
+    jz_comm (paper_2604_05885_b200.dist). Device time per step = max over ranks (CUDA events on
+    each rank's stream); e2e = the same with each rank's slice copied from pinned host memory and
+    its rows copied back every step."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2604_05885_b200 import _binding as B
+    from paper_2604_05885_b200.dist import Comm, dist_knn
+    from synth import CONFIGS, make_config
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local_rank)
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local_rank))
+    c = CONFIGS[args.config]
+    n = args.n or c["n"]
+    lo, hi = (n * rank) // world, (n * (rank + 1)) // world
+    pos, box, k = make_config(args.config, n=n, start=lo, stop=hi)
+    d_pos = torch.from_numpy(pos).cuda()
+    comm = Comm.from_torch()
+    order = args.order or "z"
+    st = torch.cuda.current_stream()
+    stats = {}
+
+    def step(p=d_pos):
+        return dist_knn(p, lo, k, box, comm, order=order, stream=st, stats=stats)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+
+    def max_all(v):
+        t = torch.tensor([float(v)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    clk = None
+    if not args.profile:
+        clk = ClockSampler(local_rank)
+        clk.start()
+    l0 = B.lib().jz_launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0.record(st)
+    for _ in range(args.steps):
+        step()
+    e1.record(st)
+    torch.cuda.synchronize()
+    dist.barrier()
+    clocks = clk.stop() if clk is not None else None
+    ms_max = max_all(e0.elapsed_time(e1) / args.steps)
+    launches = B.lib().jz_launch_count() - l0
+    e2e = None
+    if not args.no_e2e and not args.profile:
+        h_pos = torch.from_numpy(pos).pin_memory()
+        res = step(h_pos.to("cuda", non_blocking=True))
+        outs = [torch.empty(r.shape, dtype=r.dtype).pin_memory() for r in res]
+        del res
+        steps = max(1, min(args.steps, 3))
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(st)
+        h2d = d2h = 0
+        for _ in range(steps):
+            dp = h_pos.to("cuda", non_blocking=True)
+            res = step(dp)
+            for o, r in zip(outs, res):
+                o.copy_(r, non_blocking=True)
+            h2d = dp.numel() * 4
+            d2h = sum(r.numel() * r.element_size() for r in res)
+        t1.record(st)
+        torch.cuda.synchronize()
+        e2e_ms = max_all(t0.elapsed_time(t1) / steps)
+        e2e = {"value": n / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(max_all(h2d) * world),
+               "d2h_bytes_per_step": int(max_all(d2h) * world), "ms_per_step": e2e_ms,
+               "api": "jz_knn_build_dist + jz_knn_query_dist (pinned host slice per rank, rows back to pinned host)"}
+    if rank == 0:
+        line = {"metric": METRIC, "value": n / (ms_max / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": args.config, "n_points": n, "k": k, "box": "periodic L=1" if box else "open",
+                           "distribution": c["kind"],
+                           "order": "z (rows + global ids)" if order == "z" else "input (F2 reverse all-to-all-v)",
+                           "parallelism": f"Morton-range partition x{world} + ghost exchange (jz_comm over NCCL)",
+                           "l2": _l2_note(n // world, k)},
+                "rank0": stats, "gpu_launches": int(launches), "clocks": clocks, "e2e": e2e}
+        print(json.dumps(line), flush=True)
+    comm.free()
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -283,9 +384,7 @@ def main():
         return
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if world > 1 or args.dist:
-        from paper_2604_05885_b200.dist import run_bench_distributed
-
-        run_bench_distributed(args, METRIC, UNIT)
+        run_distributed(args)
     else:
         run_single(args)
 

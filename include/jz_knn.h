@@ -44,6 +44,8 @@ extern "C" {
 
 typedef struct CUstream_st *jz_stream_t; /* same type as cudaStream_t */
 typedef struct jz_knn_index jz_knn_index;  /* opaque; owns all its device memory */
+typedef struct jz_comm jz_comm;            /* opaque communicator of the multi-GPU path (one rank per GPU) */
+typedef struct jz_comm_world jz_comm_world; /* opaque in-process world of logical ranks (tests) */
 
 enum {
   JZ_OK = 0,
@@ -51,6 +53,7 @@ enum {
   JZ_EDATA = 3,     /* NaN / Inf coordinate, or periodic coordinate outside [0, L) */
   JZ_ECAPACITY = 4, /* reserved: internal capacities grow on demand */
   JZ_ECUDA = 5,     /* CUDA runtime error (message in jz_last_error) */
+  JZ_ENCCL = 6,     /* NCCL error, or libnccl.so.2 not loadable (message in jz_last_error) */
   JZ_ENOMEM = 7     /* device allocation failed */
 };
 
@@ -176,9 +179,86 @@ JZ_API int64_t jz_launch_count(void);
 JZ_API const char *jz_last_error(void);
 
 /* ---------------------------------------------------------------------------
- * Multi-GPU stage entry points. The exchanges between
- * ranks are done by the caller (torch.distributed over NCCL); these calls do
- * the per-rank compute on device buffers.
+ * Multi-GPU exact kNN (§3.3 L388-393 distributed kNN; L112-114 sample-
+ * splitter Morton-range partition; L458 z-order output).
+ * One process (or thread) per rank, each with its own device and stream. Every
+ * call below is COLLECTIVE: all ranks of the communicator must make it, in the
+ * same order. The exchanges run inside the library on a jz_comm.
+ * ------------------------------------------------------------------------- */
+
+/* NCCL bootstrap, step 1 (rank 0 only): a 128-byte NCCL unique id (host) that the
+ * caller broadcasts to the other ranks (e.g. with torch.distributed). libnccl.so.2
+ * is opened at run time (dlopen); JZ_ENCCL if it cannot be loaded. */
+JZ_API int jz_comm_unique_id(uint8_t id[128]);
+
+/* NCCL bootstrap, step 2 (every rank): communicator of nranks (1..32) ranks on the
+ * CURRENT CUDA device (ncclCommInitRank). *out is owned by the caller (jz_comm_free),
+ * must outlive every index built on it. JZ_EINVAL on bad arguments, JZ_ENCCL from NCCL. */
+JZ_API int jz_comm_init(const uint8_t id[128], int nranks, int rank, jz_comm **out);
+
+/* In-process world of nranks (1..32) logical ranks sharing one device (tests and
+ * single-GPU rehearsals of the multi-GPU path): each logical rank runs in its own
+ * host thread with its own stream and gets its communicator from jz_comm_init_local.
+ * Exchanges are device-to-device copies between the ranks' buffers. */
+JZ_API int jz_comm_local_world(int nranks, jz_comm_world **out);
+
+/* Communicator of logical rank `rank` of world w (w must outlive it). */
+JZ_API int jz_comm_init_local(jz_comm_world *w, int rank, jz_comm **out);
+
+/* rank and size (host) of a communicator. */
+JZ_API int jz_comm_rank_size(const jz_comm *c, int32_t *rank, int32_t *size);
+
+/* Release a communicator (NULL-safe; not collective for local worlds). */
+JZ_API void jz_comm_free(jz_comm *c);
+
+/* Release a local world after every communicator of it was freed (NULL-safe). */
+JZ_API void jz_comm_world_free(jz_comm_world *w);
+
+/* Distributed build (collective). This rank passes its slice of the global input:
+ * pos [n][3] float32 (device; n may be 0), global ids gidx_base .. gidx_base+n-1 (the
+ * slices of the ranks need not be contiguous for JZ_ORDER_Z; JZ_ORDER_INPUT needs
+ * the slices contiguous and in rank order). Steps inside: validation (JZ_EDATA as
+ * jz_knn_build) and one global key frame (open boundary: all-reduced bounding box,
+ * P:L133), N_samp = min(1000, 16384 / R) keys sampled per rank, all-gathered,
+ * sorted identically on every rank, R - 1 quantile splitters; Morton-range partition
+ * (a key equal to a splitter goes to the upper rank), all-to-all-v of float4 {x, y, z,
+ * bits(gidx)} rows; local tree over the received points. *out: an index of
+ * this rank's received points, bound to comm (which must outlive it); free it with
+ * jz_knn_free. JZ_EINVAL: no points on any rank, bad box or arguments. */
+JZ_API int jz_knn_build_dist(jz_comm *comm, const float *pos, int64_t n, int64_t gidx_base, const float *box,
+                             const jz_knn_params *p, jz_stream_t s, jz_knn_index **out);
+
+/* Rows (host) that jz_knn_query_dist writes on this rank: JZ_ORDER_Z = the points
+ * this rank received in the partition; JZ_ORDER_INPUT = n of its own input slice. */
+JZ_API int jz_knn_rows_dist(const jz_knn_index *ix, int order, int64_t *m);
+
+/* Distributed query (collective), exact for any 1 <= k <= total points: rows ordered
+ * (d2, global index), self included, bit-identical to the single-GPU jz_knn_query
+ * over the union. Steps inside: (1) walk over the local points: exact
+ * local rows whose k-th d2 bounds the global k-th d2; (2) query boxes = the nodes of
+ * the finest plane with <= 4096 nodes, radius^2 = the largest local k-th d2 inside,
+ * all-gathered; (3) each rank sends every point within a peer box's radius (exact
+ * point-box bound) with an all-to-all-v, and the boxes some point reached are
+ * all-reduced; (4) only the queries of reached boxes are walked again over local +
+ * ghost points and their rows replaced (P:L388-393 remote data). JZ_ORDER_Z: rows
+ * [m][k] (m = jz_knn_rows_dist) in z order of this rank's points, out_row_gidx [m]
+ * their global ids. JZ_ORDER_INPUT: rows [n][k] of the own input slice in
+ * input order (reverse all-to-all-v); out_row_gidx optional.
+ * out_idx int32 global ids, out_d2 float32 canonical d2 (device, caller-owned). */
+JZ_API int jz_knn_query_dist(jz_knn_index *ix, int k, int order, int32_t *out_idx, float *out_d2,
+                             int32_t *out_row_gidx, jz_stream_t s);
+
+/* Counters / wall times (host) of this rank's last distributed build + query:
+ * counts = {local points, ghost points received, queries walked twice, query boxes};
+ * ms = {frame + partition, local build, local walk, boxes + ghosts + second walk,
+ * reverse exchange, device-busy time of this logical rank accumulated since its
+ * communicator was created (worlds made with JZ_LOCAL_SERIAL=1 run the ranks' device
+ * work one rank at a time, so this is the uncontended per-rank time; 0 for NCCL)}. */
+JZ_API int jz_knn_dist_stats(const jz_knn_index *ix, int64_t counts[4], double ms[6]);
+
+/* ---------------------------------------------------------------------------
+ * Multi-GPU stage entry points (per-rank compute on device buffers, used by
+ * jz_knn_build_dist / jz_knn_query_dist and exposed for tests and tools).
  * ------------------------------------------------------------------------- */
 
 /* Morton keys of n points in a given frame (origin[3], extent; periodic: pass the

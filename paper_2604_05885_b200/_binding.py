@@ -12,7 +12,7 @@ import torch
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libjzknn.so")
 
-JZ_OK, JZ_EINVAL, JZ_EDATA, JZ_ECAPACITY, JZ_ECUDA, JZ_ENOMEM = 0, 2, 3, 4, 5, 7
+JZ_OK, JZ_EINVAL, JZ_EDATA, JZ_ECAPACITY, JZ_ECUDA, JZ_ENCCL, JZ_ENOMEM = 0, 2, 3, 4, 5, 6, 7
 JZ_ORDER_INPUT, JZ_ORDER_Z = 0, 1
 JZ_FLAG_FRAME, JZ_FLAG_NO_EARLY_EXIT, JZ_FLAG_NO_SEGSORT, JZ_FLAG_QBOX_DIAG = 1, 2, 4, 8
 
@@ -23,6 +23,9 @@ EXPORTS = [
     "jz_pack_by_rank", "jz_knn_plane_nodes", "jz_knn_query_boxes", "jz_knn_select_ghosts", "jz_knn_pack_ghosts",
     "jz_knn_debug_copy", "jz_launch_count", "jz_knn_stats", "jz_pack_rows", "jz_scatter_rows",
     "jz_fof", "jz_fof_catalogue",
+    "jz_comm_unique_id", "jz_comm_init", "jz_comm_local_world", "jz_comm_init_local", "jz_comm_rank_size",
+    "jz_comm_free", "jz_comm_world_free", "jz_knn_build_dist", "jz_knn_rows_dist", "jz_knn_query_dist",
+    "jz_knn_dist_stats",
 ]
 
 
@@ -83,6 +86,17 @@ def lib():
             "jz_scatter_rows": ([P, I64, I32, I64, I64, P, P, P], ctypes.c_int),
             "jz_fof": ([P, ctypes.c_float, I32, P, P, P], ctypes.c_int),
             "jz_fof_catalogue": ([P, I64, P, P, P, P, P], ctypes.c_int),
+            "jz_comm_unique_id": ([P], ctypes.c_int),
+            "jz_comm_init": ([P, ctypes.c_int, ctypes.c_int, P], ctypes.c_int),
+            "jz_comm_local_world": ([ctypes.c_int, P], ctypes.c_int),
+            "jz_comm_init_local": ([P, ctypes.c_int, P], ctypes.c_int),
+            "jz_comm_rank_size": ([P, P, P], ctypes.c_int),
+            "jz_comm_free": ([P], None),
+            "jz_comm_world_free": ([P], None),
+            "jz_knn_build_dist": ([P, P, I64, I64, P, P, P, P], ctypes.c_int),
+            "jz_knn_rows_dist": ([P, ctypes.c_int, P], ctypes.c_int),
+            "jz_knn_query_dist": ([P, ctypes.c_int, ctypes.c_int, P, P, P, P], ctypes.c_int),
+            "jz_knn_dist_stats": ([P, P, P], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)

@@ -17,7 +17,7 @@ BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libjzknn.so")
 ROOT = os.path.dirname(HERE)
 
-SOURCES = ["jz_scan.cu", "jz_sort.cu", "jz_build.cu", "jz_walk.cu", "jz_leaf.cu", "jz_dist.cu", "jz_api.cu"]
+SOURCES = ["jz_scan.cu", "jz_sort.cu", "jz_build.cu", "jz_walk.cu", "jz_leaf.cu", "jz_dist.cu", "jz_comm.cu", "jz_api.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -61,7 +61,7 @@ def build(verbose: bool = False, force: bool = False, extra=(), out: str = LIB, 
     if not os.path.exists(out) or os.path.getmtime(out) < max(os.path.getmtime(o) for o in objs):
         tmp = out + f".tmp{os.getpid()}"
         cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC",
-               "-cudart=static", "-o", tmp, *objs]
+               "-cudart=static", "-o", tmp, *objs, "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

@@ -7,37 +7,14 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <ctime>
 #include <string>
 #include <vector>
 
 #include "jz_common.cuh"
 #include "jz_internal.h"
 
-struct jz_knn_index {
-  cudaStream_t st = nullptr;
-  int64_t n = 0, n_query = 0, n_src = 0;
-  jz::Dom D{};
-  jz_knn_params prm{};
-  float4 *pts = nullptr;     // all points, z order (.w = gidx; < 0: query-only point)
-  uint64_t *keys = nullptr;
-  int32_t *perm = nullptr;   // z position -> input position
-  // type-separated views: alias pts / leaf beg / perm when every point is both
-  float4 *spts = nullptr, *qpts = nullptr;
-  int32_t *sbeg = nullptr, *qbeg = nullptr, *qin = nullptr;
-  bool own_s = false, own_q = false;
-  bool input_ids = false;  // point ids are input positions 0..n-1 (jz_knn_build): needed by jz_fof
-  std::vector<jz::Plane> planes;
-  cudaEvent_t ev[8] = {};
-  bool timing = false;
-  float times[6] = {0, 0, 0, 0, 0, 0};
-  long long evals = 0, inserts = 0;
-  long long walk[5] = {0, 0, 0, 0, 0};  // entries, warp-passed leaves, staged leaves, flush rounds, work items
-  unsigned long long *d_evals = nullptr;
-  // friends-of-friends catalogue of the last jz_fof call (device; group order = root z-order)
-  int64_t fof_ngroups = 0;
-  int32_t *fof_label = nullptr, *fof_count = nullptr;
-  double *fof_com = nullptr, *fof_rad = nullptr;
-};
+
 
 #include <atomic>
 
@@ -340,8 +317,10 @@ __global__ void k_fof_cat(const float4 *__restrict__ pts, const int32_t *__restr
   }
 }
 
-jz_knn_index *build_impl(const float *pos, int64_t n, int stride, int gidx_mode, int64_t n_query, const float *box,
-                         const jz_knn_params *p, cudaStream_t st) {
+}  // namespace
+
+jz_knn_index *jz::build_impl(const float *pos, int64_t n, int stride, int gidx_mode, int64_t n_query, const float *box,
+                             const jz_knn_params *p, cudaStream_t st) {
   if (!pos) throw jz::Error(JZ_EINVAL, "pos is NULL");
   if (n < 1 || n > (int64_t)INT32_MAX - 1) throw jz::Error(JZ_EINVAL, "n must be in [1, 2^31 - 2]");
   if (n_query < 0 || n_query > n) throw jz::Error(JZ_EINVAL, "n_query must be in [0, n]");
@@ -363,17 +342,36 @@ jz_knn_index *build_impl(const float *pos, int64_t n, int stride, int gidx_mode,
   try {
     if (ix->timing)
       for (auto &e : ix->ev) JZ_CUDA(cudaEventCreate(&e));
+    static const bool bprof = getenv("JZ_BUILD_PROF") != nullptr;
+    timespec tq;
+    auto wall = [&]() {
+      clock_gettime(CLOCK_MONOTONIC, &tq);
+      return tq.tv_sec * 1e3 + tq.tv_nsec * 1e-6;
+    };
+    double tb = wall();
+    auto bmark = [&](const char *w) {  // diagnostics: host wall time of each build step
+      if (!bprof) return;
+      cudaStreamSynchronize(st);
+      const double t = wall();
+      fprintf(stderr, "build n=%lld %-8s %8.2f ms\n", (long long)n, w, t - tb);
+      tb = t;
+    };
     rec(ix, 0);
     jz::Frame frame;
     jz::compute_frame(pos, n, stride, ix->D, prm, &frame, st);
+    bmark("frame");
     rec(ix, 1);
     JZ_CUDA(cudaMallocAsync(&ix->pts, n * sizeof(float4), st));
     JZ_CUDA(cudaMallocAsync(&ix->keys, n * sizeof(uint64_t), st));
     JZ_CUDA(cudaMallocAsync(&ix->perm, n * sizeof(int32_t), st));
+    bmark("alloc");
     jz::sort_points(pos, n, stride, gidx_mode, 0, frame, ix->keys, ix->perm, ix->pts, st);
+    bmark("sort");
     rec(ix, 2);
     jz::build_planes(ix->keys, ix->pts, n, prm, ix->planes, st);
+    bmark("planes");
     split_types(ix, gidx_mode != 0);
+    bmark("types");
     rec(ix, 3);
     if (ix->timing) {
       JZ_CUDA(cudaEventSynchronize(ix->ev[3]));
@@ -388,8 +386,6 @@ jz_knn_index *build_impl(const float *pos, int64_t n, int stride, int gidx_mode,
   }
   return ix;
 }
-
-}  // namespace
 
 namespace jz {
 void set_last_error(const std::string &m) { g_err = m; }
@@ -421,7 +417,7 @@ int jz_knn_build(const float *pos, int64_t n, const float *box, const jz_knn_par
                  jz_knn_index **out) {
   JZ_API_BEGIN
   if (!out) return fail(JZ_EINVAL, "out is NULL");
-  *out = build_impl(pos, n, 3, 0, n, box, p, (cudaStream_t)s);
+  *out = jz::build_impl(pos, n, 3, 0, n, box, p, (cudaStream_t)s);
   return JZ_OK;
   JZ_API_END
 }
@@ -430,7 +426,7 @@ int jz_knn_build_xyzg(const float *pts4, int64_t n, int64_t n_query, const float
                       jz_stream_t s, jz_knn_index **out) {
   JZ_API_BEGIN
   if (!out) return fail(JZ_EINVAL, "out is NULL");
-  *out = build_impl(pts4, n, 4, 1, n_query, box, p, (cudaStream_t)s);
+  *out = jz::build_impl(pts4, n, 4, 1, n_query, box, p, (cudaStream_t)s);
   return JZ_OK;
   JZ_API_END
 }
@@ -448,7 +444,7 @@ int jz_knn_build_xq(const float *src, int64_t n_src, const float *qry, int64_t n
   k_pack_xq<<<jz::grid_for(n_src + n_qry, 256), 256, 0, st>>>(qry, n_qry, src, n_src, tmp);
   JZ_LAUNCH_CHECK();
   try {
-    *out = build_impl(reinterpret_cast<const float *>(tmp), n_src + n_qry, 4, 1, n_qry, box, p, st);
+    *out = jz::build_impl(reinterpret_cast<const float *>(tmp), n_src + n_qry, 4, 1, n_qry, box, p, st);
   } catch (...) {
     cudaFreeAsync(tmp, st);
     throw;

@@ -9,6 +9,8 @@
 
 typedef jz_knn_params jz_knn_params_t;
 
+
+
 namespace jz {
 
 // One tree plane (a set of nodes partitioning the points).
@@ -29,12 +31,53 @@ struct Stage {
   bool on = false;
 };
 
+}  // namespace jz
+
+// the index behind the C ABI's opaque jz_knn_index (jz_api.cu; multi-GPU fields: jz_dist.cu)
+struct jz_knn_index {
+  cudaStream_t st = nullptr;
+  int64_t n = 0, n_query = 0, n_src = 0;
+  jz::Dom D{};
+  jz_knn_params prm{};
+  float4 *pts = nullptr;     // all points, z order (.w = gidx; < 0: query-only point)
+  uint64_t *keys = nullptr;
+  int32_t *perm = nullptr;   // z position -> input position
+  // type-separated views: alias pts / leaf beg / perm when every point is both
+  float4 *spts = nullptr, *qpts = nullptr;
+  int32_t *sbeg = nullptr, *qbeg = nullptr, *qin = nullptr;
+  bool own_s = false, own_q = false;
+  bool input_ids = false;  // point ids are input positions 0..n-1 (jz_knn_build): needed by jz_fof
+  std::vector<jz::Plane> planes;
+  cudaEvent_t ev[8] = {};
+  bool timing = false;
+  float times[6] = {0, 0, 0, 0, 0, 0};
+  long long evals = 0, inserts = 0;
+  long long walk[5] = {0, 0, 0, 0, 0};  // entries, warp-passed leaves, staged leaves, flush rounds, work items
+  unsigned long long *d_evals = nullptr;
+  // friends-of-friends catalogue of the last jz_fof call (device; group order = root z-order)
+  int64_t fof_ngroups = 0;
+  int32_t *fof_label = nullptr, *fof_count = nullptr;
+  double *fof_com = nullptr, *fof_rad = nullptr;
+  // multi-GPU (jz_knn_build_dist): this rank's part of a distributed index (jz_dist.cu)
+  jz_comm *comm = nullptr;
+  int64_t n_own = 0, gidx_base = 0;  // this rank's input slice: global ids [gidx_base, gidx_base + n_own)
+  bool has_box = false;
+  float box[3] = {0, 0, 0};
+  jz_knn_params prm_frame{};         // params with the global key frame (open boundary: JZ_FLAG_FRAME)
+  bool empty = false;                // no local points after the partition (no tree)
+  double dist_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // phase wall times of the last build / query
+  int64_t dist_cnt[4] = {0, 0, 0, 0};          // local points, ghosts received, re-queried, boxes
+};
+
+namespace jz {
+
 // build (jz_sort.cu)
 void compute_frame(const float *pos, int64_t n, int stride, const Dom &D, const jz_knn_params_t &prm, Frame *frame,
                    cudaStream_t st);
 void sort_points(const float *pos, int64_t n, int stride, int gidx_mode, int64_t gidx_base, const Frame &frame,
                  uint64_t *keys_out, int32_t *perm_out, float4 *pts_out, cudaStream_t st);
 void morton_keys(const float *pos, int64_t n, const Frame &f, uint64_t *keys, cudaStream_t st);
+void local_bbox(const float *pos, int64_t n, int stride, const Dom &D, float lo[3], float hi[3], cudaStream_t st);
 
 // tree (jz_build.cu)
 void build_planes(const uint64_t *keys, const float4 *pts, int64_t n, const jz_knn_params_t &prm,
@@ -98,6 +141,10 @@ struct IndexView {
   unsigned flags;
 };
 IndexView view_of(const jz_knn_index *ix);
+
+// A1-A8 build of an index (jz_api.cu): stride 3 (xyz) or 4 (xyzg with gidx_mode = 1)
+jz_knn_index *build_impl(const float *pos, int64_t n, int stride, int gidx_mode, int64_t n_query, const float *box,
+                         const jz_knn_params *p, cudaStream_t st);
 
 // text returned by jz_last_error() (thread-local)
 void set_last_error(const std::string &m);

@@ -602,6 +602,38 @@ void compute_frame(const float *pos, int64_t n, int stride, const Dom &D, const 
   }
 }
 
+// validation + bounding box of this rank's points (multi-GPU frame: all-reduced by the caller);
+// n = 0: lo = +inf, hi = -inf
+void local_bbox(const float *pos, int64_t n, int stride, const Dom &D, float lo[3], float hi[3], cudaStream_t st) {
+  for (int d = 0; d < 3; ++d) {
+    lo[d] = INFINITY;
+    hi[d] = -INFINITY;
+  }
+  if (n <= 0) return;
+  FrameStats h;
+  for (int d = 0; d < 3; ++d) {
+    h.lo[d] = 0xffffffffu;
+    h.hi[d] = 0u;
+  }
+  h.bad = 0;
+  FrameStats *dst = nullptr;
+  JZ_CUDA(cudaMallocAsync(&dst, sizeof(FrameStats), st));
+  JZ_CUDA(cudaMemcpyAsync(dst, &h, sizeof(h), cudaMemcpyHostToDevice, st));
+  k_frame<<<grid_for(n, 256, 148 * 8), 256, 0, st>>>(pos, n, stride, D, dst);
+  JZ_LAUNCH_CHECK();
+  JZ_CUDA(cudaMemcpyAsync(&h, dst, sizeof(h), cudaMemcpyDeviceToHost, st));
+  JZ_CUDA(cudaFreeAsync(dst, st));
+  JZ_CUDA(cudaStreamSynchronize(st));
+  if (h.bad & 1) throw Error(3, "non-finite coordinate in input");
+  if (h.bad & 2) throw Error(3, "periodic coordinate outside [0, L)");
+  for (int d = 0; d < 3; ++d) {
+    const unsigned a = (h.lo[d] & 0x80000000u) ? (h.lo[d] & 0x7fffffffu) : ~h.lo[d];
+    const unsigned b = (h.hi[d] & 0x80000000u) ? (h.hi[d] & 0x7fffffffu) : ~h.hi[d];
+    memcpy(&lo[d], &a, 4);
+    memcpy(&hi[d], &b, 4);
+  }
+}
+
 // 8-pass sort of the full 63-bit keys (fallback for runs of equal high keys > kSegBlock)
 static void sort_points8(const float *pos, int64_t n, int stride, int gidx_mode, int64_t gidx_base, const Frame &frame,
                          uint64_t *keys_out, int32_t *perm_out, float4 *pts_out, cudaStream_t st) {

@@ -1,10 +1,7 @@
-"""CPU stand-in for the per-rank GPU stages of paper_2604_05885_b200.dist (TEST ONLY).
-
-It lets the real multi-GPU orchestration (dist_knn: splitters, bucketing, count exchange,
-all-to-all-v, query boxes, ghost protocol, z-order rows) run over torch.distributed/gloo on
-CPU. Every stage is a plain numpy / oracle computation; the final per-rank kNN is the oracle's
-brute force over local + ghost points, so the gathered result equals the global oracle only
-if the ghost protocol delivered every needed point.
+"""CPU stand-ins for the per-rank stages of the library's distributed kNN (TEST ONLY), used by
+the protocol model tests/dist_model.py over torch.distributed / gloo. Every stage is a plain
+numpy / oracle computation; the per-rank kNN is the oracle's brute force, so the gathered result
+equals the global oracle only if the ghost protocol delivered every needed point.
 """
 import numpy as np
 import torch
@@ -57,33 +54,35 @@ class CpuBackend:
         return torch.from_numpy(np.concatenate([p, g[:, None]], axis=1).astype(np.float32))
 
     def build(self, pts4, n_query, box):
-        return CpuIndex(pts4, n_query, box)
+        """Local points sorted into z order (the library's index order)."""
+        p = pts4.cpu().numpy()
+        if p.shape[0]:
+            o, s = T.key_frame(p[:, :3], box) if box is not None else T.key_frame(p[:, :3])
+            p = p[np.argsort(T.morton_keys(T.quantize(p[:, :3], o, s, is_scale=True)), kind="stable")]
+        return CpuIndex(torch.from_numpy(np.ascontiguousarray(p)), n_query, box)
 
-    def query_boxes(self, ix, k, rank):
-        """Chunks of 64 local points (key order): AABB + max local k-th d2 (a valid bound:
-        the local k-th distance can only shrink when more points are added)."""
+    def query_boxes(self, ix, k, rank, d2=None):
+        """Chunks of 64 local points (key order): AABB + max local k-th d2 (a valid bound: the
+        local k-th distance can only shrink when more points are added); +inf without local rows
+        (d2 None). Returns the boxes and the local rows (point indices) inside each box."""
         p = ix.pts4[:, :3]
         n = p.shape[0]
-        if n < k:
-            r2 = np.full(n, np.inf)
-        else:
-            _, d2 = knn_brute(p, k, ix.box)
-            r2 = d2[:, -1].astype(np.float64)
-        o, s = T.key_frame(p, ix.box) if ix.box is not None else T.key_frame(p)
-        order = np.argsort(T.morton_keys(T.quantize(p, o, s, is_scale=True)), kind="stable")
-        rows = []
-        for c in range(0, n, 64):
-            sel = order[c:c + 64]
+        r2 = np.full(n, np.inf) if d2 is None else d2.numpy()[:, -1].astype(np.float64)
+        rows, members = [], []
+        for c in range(0, n, 64):  # ix.pts4 rows are the local points in z order
+            sel = np.arange(c, min(n, c + 64))
             lo, hi = p[sel].min(0), p[sel].max(0)
-            rows.append([*lo, r2[sel].max(), *hi, np.float32(rank).view(np.int32).view(np.float32)])
-        out = np.asarray(rows, np.float32)
+            rows.append([*lo, r2[sel].max(), *hi, 0.0])
+            members.append(sel)
+        out = np.asarray(rows, np.float32).reshape(-1, 8)
         out[:, 7] = np.array([rank] * len(rows), np.int32).view(np.float32)
-        return torch.from_numpy(out)
+        return torch.from_numpy(out), members
 
     def select_ghosts(self, ix, boxes, rank, R):
         b = boxes.numpy()
         p = ix.pts4[:, :3].astype(np.float64)
         mask = np.zeros(ix.n, np.int32)
+        hitbox = np.zeros(b.shape[0], np.int32)
         rk = b[:, 7].view(np.int32)
         for j in range(b.shape[0]):
             if rk[j] == rank:
@@ -101,8 +100,9 @@ class CpuBackend:
             r = np.sqrt(np.float64(b[j, 3]))
             hit = d <= r * (1 + 1e-5) + 1e-7
             mask[hit] |= 1 << int(rk[j])
+            hitbox[j] = int(hit.any())
         counts = [int(((mask >> r) & 1).sum()) for r in range(R)]
-        return torch.from_numpy(mask), counts
+        return torch.from_numpy(mask), counts, hitbox
 
     def pack_ghosts(self, ix, mask, counts):
         m = mask.numpy()

@@ -1,8 +1,10 @@
-"""World-size-2/3 gloo tests (CPU) of the multi-GPU orchestration in
-paper_2604_05885_b200.dist: sample splitters, Morton-range redistribution, query boxes and the
-ghost exchange, z-order rows with global ids. The per-rank stages are the CPU stand-ins of
-tests/cpu_backend.py; the gathered result must equal the oracle on the whole set (rank
-transparency)."""
+"""World-size-2/3 gloo tests (CPU) of the distributed-kNN protocol that jz_knn_build_dist /
+jz_knn_query_dist run inside the library: sample splitters, Morton-range redistribution, query
+boxes from the local k-th distances, ghost exchange with reached-box flags, re-walk of the
+reached queries, z-order rows with global ids (tests/dist_model.py restates the protocol over
+gloo with the CPU stand-ins of tests/cpu_backend.py). The gathered result must equal the
+oracle on the whole set (rank transparency). The library's own
+implementation is tested with logical ranks on the GPU (tests/test_gpu_dist.py)."""
 import os
 import socket
 import tempfile
@@ -27,8 +29,8 @@ def _free_port():
 def _worker(rank, world, port, n, kind, box, k, out_dir, order="z"):
     import torch.distributed as dist
 
-    from paper_2604_05885_b200.dist import TorchComm, dist_knn
     from tests.cpu_backend import CpuBackend
+    from tests.dist_model import TorchComm, dist_knn_model
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -38,7 +40,7 @@ def _worker(rank, world, port, n, kind, box, k, out_dir, order="z"):
     pos = torch.from_numpy(gen(n, 7, 1.0, start=lo, stop=hi))
     if kind == "octant":  # adversarial: everything in one corner, ranks hold each other's neighbours
         pos = pos * 0.125
-    idx, d2, rowg = dist_knn(pos, lo, k, box, TorchComm(), CpuBackend(), n_samp=64, seed=3, order=order)
+    idx, d2, rowg = dist_knn_model(pos, lo, k, box, TorchComm(), CpuBackend(), n_samp=64, seed=3, order=order)
     if order == "input":  # F2: this rank's own input slice, in input order
         assert rowg.tolist() == list(range(lo, hi))
     np.savez(os.path.join(out_dir, f"r{rank}.npz"), idx=idx.numpy(), d2=d2.numpy(), rowg=rowg.numpy())
@@ -84,9 +86,9 @@ def test_gloo_dist_knn_input_order(world):
 
 
 def test_splitters_quantiles():
-    from paper_2604_05885_b200.dist import splitters_from_samples
+    from tests.dist_model import splitters_from_samples
 
     s = torch.arange(100, dtype=torch.int64).flip(0)
-    spl = splitters_from_samples(s, 4, lambda x: torch.sort(x).values)
+    spl = splitters_from_samples(s, 4)
     assert spl.tolist() == [25, 50, 75]
-    assert splitters_from_samples(s, 1, lambda x: torch.sort(x).values).numel() == 0
+    assert splitters_from_samples(s, 1).numel() == 0

@@ -1,7 +1,9 @@
-"""Multi-GPU path on one B200: R logical ranks (threads, in-process exchange) drive every
-per-rank stage kernel (Morton keys, splitter bucketing, packing, query boxes, ghost
-selection and packing, ghost-carrying build, z-order query) exactly as under torchrun.
-Gathered rows must equal the oracle for every R (rank transparency)."""
+"""Multi-GPU path on one B200: the library's distributed kNN (jz_knn_build_dist /
+jz_knn_query_dist) on R logical ranks (threads, the library's in-process communicator) runs the
+same code as under torchrun with NCCL: global frame, sampled splitters, Morton-range exchange,
+local walk, query boxes from the local k-th distances, ghost exchange, re-walk of the reached
+queries, z-order rows (or input order, F2). Gathered rows must equal the oracle for every R
+(rank transparency). The NCCL communicator itself runs at one rank."""
 import numpy as np
 import pytest
 
@@ -68,3 +70,63 @@ def test_scatter_rows_rejects_foreign_rows():
     od = torch.empty((5, 2), dtype=torch.float32, device="cuda")
     rc = B.lib().jz_scatter_rows(B.dptr(rows), 2, 2, 10, 5, B.dptr(oi), B.dptr(od), None)
     assert rc == B.JZ_EDATA and b"outside" in B.lib().jz_last_error()
+
+
+def test_nccl_comm_one_rank():
+    """The NCCL communicator (jz_comm_unique_id / jz_comm_init, libnccl loaded at run time) at
+    one rank: the distributed entry points give the single-GPU rows."""
+    import ctypes
+
+    import torch
+
+    from paper_2604_05885_b200 import _binding as B
+    from paper_2604_05885_b200.dist import Comm, dist_knn
+
+    uid = (ctypes.c_uint8 * 128)()
+    B.check(B.lib().jz_comm_unique_id(uid))
+    h = ctypes.c_void_p()
+    B.check(B.lib().jz_comm_init(uid, 1, 0, ctypes.byref(h)))
+    comm = Comm(h)
+    pos = clustered_points(50_000, 31, 1.0)
+    for order in ("z", "input"):
+        idx, d2, rowg = dist_knn(torch.from_numpy(pos).cuda(), 0, 16, 1.0, comm, order=order)
+        io, do = knn_grid(pos, 16, 1.0)
+        g = rowg.cpu().numpy()
+        assert np.array_equal(idx.cpu().numpy(), io[g]) and np.array_equal(d2.cpu().numpy(), do[g])
+    comm.free()
+
+
+def test_dist_ghost_protocol_counts():
+    """Ghosts come from the exact local k-th radii (not the count-heap R_max): on the C4
+    distribution at R = 8 every rank receives far fewer ghosts than it holds, and only the
+    queries of reached boxes are walked twice; rows stay exact."""
+    from paper_2604_05885_b200.dist import run_ranks_simulated
+
+    pos = clustered_points(400_000, 37, 1.0)
+    stats = []
+    idx, d2, owned = run_ranks_simulated(pos, 16, 1.0, 8, stats=stats)
+    io, do = knn_grid(pos, 16, 1.0)
+    assert np.array_equal(idx, io) and np.array_equal(d2.view(np.int32), do.view(np.int32))
+    for _, s in stats:
+        assert s["n_local"] > 0 and s["n_ghost"] < s["n_local"] and s["n_requery"] <= s["n_local"]
+
+
+def test_dist_fewer_than_k_on_a_rank():
+    """A rank holding fewer than k points (tiny input split over 8 ranks) answers every query
+    through the ghost re-walk (its query boxes have an unbounded radius)."""
+    from paper_2604_05885_b200.dist import run_ranks_simulated
+
+    pos = uniform_points(40, 41, 1.0)
+    idx, d2, owned = run_ranks_simulated(pos, 12, 1.0, 8)
+    io, do = knn_grid(pos, 12, 1.0)
+    assert np.array_equal(idx, io) and np.array_equal(d2, do)
+
+
+def test_dist_bad_input_fails_on_every_rank():
+    """A NaN on one rank: that rank reports JZ_EDATA and the peers are released (no hang)."""
+    from paper_2604_05885_b200.dist import run_ranks_simulated
+
+    pos = uniform_points(1000, 43, 1.0)
+    pos[700, 1] = np.nan
+    with pytest.raises(Exception):
+        run_ranks_simulated(pos, 4, 1.0, 4)
