@@ -477,7 +477,8 @@ int jz_knn_query(jz_knn_index *ix, int k, int order, int32_t *out_idx, float *ou
   float *rmax2 = nullptr;
   int32_t *superbeg = nullptr;
   // walk down to plane 1: its nodes are the receiving parents of LeafToLeaf (jz_leaf.cu)
-  jz::walk_to(ix->planes, ix->D, k, ix->prm.ngr, ix->prm.flags, 1, il, &rmax2, &superbeg, st);
+  jz::walk_to(ix->planes, ix->D, k, ix->prm.ngr, ix->prm.flags, 1, il, &rmax2, &superbeg, st, -1.f,
+              ix->n_query < ix->n ? ix->qbeg : nullptr);
   rec(ix, 5);
   if (!ix->d_evals) JZ_CUDA(cudaMallocAsync(&ix->d_evals, 16 * sizeof(unsigned long long), st));
   JZ_CUDA(cudaMemsetAsync(ix->d_evals, 0, 16 * sizeof(unsigned long long), st));

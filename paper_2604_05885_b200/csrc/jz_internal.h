@@ -98,10 +98,13 @@ struct IList {
 // one-plane tree and stop = 1), the receivers are the super nodes: *superbeg (first top
 // node of each super node, caller frees) is set, the list is the dense one and
 // *rmax2 = nullptr (= +inf).
+// qbeg (optional): query leaf starts when the queries are a subset of the points -- receivers
+// without queries get no list.
 // fixed_r2 >= 0: fixed-radius walk (friends-of-friends): no FindRmax, every node's radius^2 is
 // fixed_r2, so the lists hold the pairs with d_low^2 <= fixed_r2.
 void walk_to(const std::vector<Plane> &planes, const Dom &D, int k, int ngr, unsigned flags, int stop, IList &il,
-             float **rmax2, int32_t **superbeg, cudaStream_t st, float fixed_r2 = -1.f);
+             float **rmax2, int32_t **superbeg, cudaStream_t st, float fixed_r2 = -1.f,
+             const int32_t *qbeg = nullptr);
 
 // leaf-to-leaf (jz_leaf.cu)
 struct LeafArgs {

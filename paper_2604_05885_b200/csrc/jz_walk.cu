@@ -125,7 +125,10 @@ __global__ void __launch_bounds__(kN2NWarps * 32) k_n2n(const int32_t *__restric
                                                        const NodeBox *__restrict__ cbox, Dom D, int k, int sorted,
                                                        int early, float *__restrict__ rmax2, int32_t *__restrict__ cnt,
                                                        const int64_t *__restrict__ ispl_out,
-                                                       int32_t *__restrict__ isrc_out, float *__restrict__ rlow_out) {
+                                                       int32_t *__restrict__ isrc_out, float *__restrict__ rlow_out,
+                                                       const uint8_t *__restrict__ qf) {
+  // qf (optional): receivers holding at least one query; the others get no list (joint trees
+  // of separate / partial query sets: source-only nodes never receive)
   __shared__ NodeBox s_box[kN2NWarps][kN2NWStage];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t J = (int64_t)blockIdx.x * kN2NWarps + warp;
@@ -135,7 +138,8 @@ __global__ void __launch_bounds__(kN2NWarps * 32) k_n2n(const int32_t *__restric
   const int64_t eb = ispl[J], ee = ispl[J + 1];
   for (int c0 = cb; c0 < ce; c0 += 32) {
     const int i = c0 + lane;
-    const bool valid = i < ce;
+    const bool inrange = i < ce;
+    const bool valid = inrange && (!qf || qf[i]);
     NodeBox mb;
     if (valid) mb = cbox[i];
     CountHeap h;
@@ -198,10 +202,24 @@ __global__ void __launch_bounds__(kN2NWarps * 32) k_n2n(const int32_t *__restric
         }
       }
     }
-    if (valid) {
-      if (MODE == RMAX) rmax2[i] = R;
-      if (MODE == COUNT) cnt[i] = count;
+    if (inrange) {
+      if (MODE == RMAX) rmax2[i] = valid ? R : 0.f;
+      if (MODE == COUNT) cnt[i] = valid ? count : 0;
     }
+  }
+}
+
+// receivers holding queries: leaves from the query leaf starts, upper planes by OR over children
+__global__ void k_qflag_leaf(const int32_t *__restrict__ qbeg, int64_t n, uint8_t *__restrict__ f) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    f[i] = qbeg[i + 1] > qbeg[i];
+}
+__global__ void k_qflag_up(const int32_t *__restrict__ beg, int64_t n, const uint8_t *__restrict__ fc,
+                           uint8_t *__restrict__ f) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint8_t v = 0;
+    for (int c = beg[i]; c < beg[i + 1] && !v; ++c) v = fc[c];
+    f[i] = v;
   }
 }
 
@@ -257,8 +275,18 @@ __global__ void k_fill_f32(float *__restrict__ a, int64_t m, float v) {
 }
 
 void walk_to(const std::vector<Plane> &planes, const Dom &D, int k, int ngr, unsigned flags, int stop, IList &out_il,
-             float **rmax2_out, int32_t **superbeg_out, cudaStream_t st, float fixed_r2) {
+             float **rmax2_out, int32_t **superbeg_out, cudaStream_t st, float fixed_r2, const int32_t *qbeg) {
   const int P = (int)planes.size();
+  // query-holding receivers per plane (only when the queries are a subset of the points)
+  std::vector<uint8_t *> qf(P, nullptr);
+  if (qbeg) {
+    for (int p = 0; p < P; ++p) {
+      JZ_CUDA(cudaMallocAsync(&qf[p], planes[p].nnodes > 0 ? planes[p].nnodes : 1, st));
+      if (p == 0) k_qflag_leaf<<<grid_for(planes[0].nnodes, 256), 256, 0, st>>>(qbeg, planes[0].nnodes, qf[0]);
+      else k_qflag_up<<<grid_for(planes[p].nnodes, 256), 256, 0, st>>>(planes[p].beg, planes[p].nnodes, qf[p - 1], qf[p]);
+      JZ_LAUNCH_CHECK();
+    }
+  }
   const int top = P - 1;
   const int64_t ntop = planes[top].nnodes;
   const int64_t S = ceil_div(ntop, ngr);
@@ -292,11 +320,11 @@ void walk_to(const std::vector<Plane> &planes, const Dom &D, int k, int ngr, uns
     } else {
       k_n2n<RMAX><<<(unsigned)ceil_div(npar, kN2NWarps), kN2NWarps * 32, 0, st>>>(pbeg, npar, il.ispl, il.isrc, il.rlow,
                                                                                 pl.box, D, k, srt, ee, rmax2, nullptr,
-                                                                                nullptr, nullptr, nullptr);
+                                                                                nullptr, nullptr, nullptr, qf[p]);
     }
     JZ_LAUNCH_CHECK();
     k_n2n<COUNT><<<(unsigned)ceil_div(npar, kN2NWarps), kN2NWarps * 32, 0, st>>>(pbeg, npar, il.ispl, il.isrc, il.rlow, pl.box, D, k, srt, ee,
-                                                         rmax2, cnt, nullptr, nullptr, nullptr);
+                                                         rmax2, cnt, nullptr, nullptr, nullptr, qf[p]);
     JZ_LAUNCH_CHECK();
     IList nl;
     nl.nrecv = pl.nnodes;
@@ -306,7 +334,7 @@ void walk_to(const std::vector<Plane> &planes, const Dom &D, int k, int ngr, uns
     JZ_CUDA(cudaMallocAsync(&nl.isrc, (nl.total > 0 ? nl.total : 1) * sizeof(int32_t), st));
     JZ_CUDA(cudaMallocAsync(&nl.rlow, (nl.total > 0 ? nl.total : 1) * sizeof(float), st));
     k_n2n<INSERT><<<(unsigned)ceil_div(npar, kN2NWarps), kN2NWarps * 32, 0, st>>>(pbeg, npar, il.ispl, il.isrc, il.rlow, pl.box, D, k, srt, ee,
-                                                          rmax2, nullptr, nl.ispl, nl.isrc, nl.rlow);
+                                                          rmax2, nullptr, nl.ispl, nl.isrc, nl.rlow, qf[p]);
     JZ_LAUNCH_CHECK();
     if (do_sort) {
       k_segsort<<<grid_for(pl.nnodes, kSegWarps, 148 * 16), kSegWarps * 32, 0, st>>>(nl.ispl, nl.nrecv, nl.isrc,
@@ -317,6 +345,8 @@ void walk_to(const std::vector<Plane> &planes, const Dom &D, int k, int ngr, uns
     il = nl;
     JZ_CUDA(cudaFreeAsync(cnt, st));
   }
+  for (auto *f : qf)
+    if (f) JZ_CUDA(cudaFreeAsync(f, st));
   out_il = il;
   *rmax2_out = rmax2;
   if (stop > top) {
