@@ -239,7 +239,11 @@ def run_single(args):
 
 
 def run_e2e(args, pos, box, k):
-    """Same metric through jz_knn_search_host: pinned host input, H2D + build + query + D2H."""
+    """Same metric end to end through the public API with pinned host buffers: H2D of the positions,
+    build, query, D2H of the rows, every step. Headline: jz_knn_search_host_z (rows in z order with
+    their input ids, streamed to the host in 16 chunks while the walk runs); also the
+    input-order call jz_knn_search_host (rows scattered to input order on the device, one D2H at
+    the end: the transfer cannot overlap the walk)."""
     import torch
 
     import paper_2604_05885_b200 as jz
@@ -248,17 +252,26 @@ def run_e2e(args, pos, box, k):
     h_pos = torch.from_numpy(pos).pin_memory()
     h_idx = torch.empty((n, k), dtype=torch.int32).pin_memory()
     h_d2 = torch.empty((n, k), dtype=torch.float32).pin_memory()
-    a, b, c = h_pos.numpy(), h_idx.numpy(), h_d2.numpy()
-    jz.knn_host(a, k, box=box, out=(b, c))
+    h_rg = torch.empty((n,), dtype=torch.int32).pin_memory()
+    a, b, c, g = h_pos.numpy(), h_idx.numpy(), h_d2.numpy(), h_rg.numpy()
     steps = max(1, min(args.steps, 3))
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for _ in range(steps):
-        jz.knn_host(a, k, box=box, out=(b, c))
-    torch.cuda.synchronize()
-    dt = (time.perf_counter() - t0) / steps
-    return {"value": n / dt, "unit": UNIT, "h2d_bytes_per_step": int(n * 12), "d2h_bytes_per_step": int(n * k * 8),
-            "ms_per_step": dt * 1e3, "api": "jz_knn_search_host (pinned host buffers)"}
+    out = {}
+    for name, fn in (("z", lambda: jz.knn_host_z(a, k, box=box, out=(b, c, g))),
+                     ("input", lambda: jz.knn_host(a, k, box=box, out=(b, c)))):
+        fn()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            fn()
+        torch.cuda.synchronize()
+        out[name] = (time.perf_counter() - t0) / steps
+    dz, di = out["z"], out["input"]
+    return {"value": n / dz, "unit": UNIT, "h2d_bytes_per_step": int(n * 12), "d2h_bytes_per_step": int(n * k * 8 + n * 4),
+            "ms_per_step": dz * 1e3,
+            "api": "jz_knn_search_host_z (pinned host buffers; rows in z order + input ids, D2H streamed during the walk)",
+            "input_order": {"value": n / di, "unit": UNIT, "ms_per_step": di * 1e3, "h2d_bytes_per_step": int(n * 12),
+                            "d2h_bytes_per_step": int(n * k * 8),
+                            "api": "jz_knn_search_host (pinned host buffers; rows in input order, one D2H)"}}
 
 
 def run_distributed(args):

@@ -156,6 +156,16 @@ JZ_API int jz_knn_search_host(const float *pos_host, int64_t n, const float *box
                        int32_t *idx_host, float *d2_host, jz_stream_t s);
 
 /*
+ * End to end on HOST buffers with the rows in z order (the multi-GPU paper output form)
+ * and streamed: LeafToLeaf runs in 16 chunks of work items (contiguous z-order row ranges) and
+ * each finished chunk is copied to the host on a second stream while the next one runs, so the
+ * device-to-host transfer overlaps the walk (k > 32: one copy at the end). Row r of idx_host /
+ * d2_host [n][k] belongs to input point row_gidx_host[r] ([n]). Same errors as above.
+ */
+JZ_API int jz_knn_search_host_z(const float *pos_host, int64_t n, const float *box, const jz_knn_params *p, int k,
+                                int32_t *idx_host, float *d2_host, int32_t *row_gidx_host, jz_stream_t s);
+
+/*
  * Per-stage device timings (ms) of the last build + query on this index, for the
  * phase breakdown of PAPER.md Fig. knnsteps:
  *   [0] frame+validate [1] sort [2] tree build [3] node-to-node walk [4] leaf-to-leaf [5] total.

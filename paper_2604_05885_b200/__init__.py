@@ -182,6 +182,22 @@ def fof(pos: torch.Tensor, r_link: float, box=None, min_count: int = 20, params=
         ix.free()
 
 
+def knn_host_z(pos: np.ndarray, k: int, box=None, params=None, out=None, stream=None):
+    """End to end on host arrays with z-order rows streamed to the host during the walk
+    (jz_knn_search_host_z): (idx [n, k], d2 [n, k], row_gidx [n])."""
+    pos = np.ascontiguousarray(pos, dtype=np.float32)
+    n = pos.shape[0]
+    if out is None:
+        out = (np.empty((n, k), dtype=np.int32), np.empty((n, k), dtype=np.float32), np.empty(n, dtype=np.int32))
+    idx, d2, rg = out
+    prm = B.make_params(params)
+    B.check(B.lib().jz_knn_search_host_z(pos.ctypes.data_as(ctypes.c_void_p), n, B.box3(box), ctypes.byref(prm),
+                                         int(k), idx.ctypes.data_as(ctypes.c_void_p),
+                                         d2.ctypes.data_as(ctypes.c_void_p), rg.ctypes.data_as(ctypes.c_void_p),
+                                         B.stream_ptr(stream)))
+    return idx, d2, rg
+
+
 def knn_host(pos: np.ndarray, k: int, box=None, params=None, out=None, stream=None):
     """End to end on host arrays through jz_knn_search_host (H2D, build, query, D2H)."""
     pos = np.ascontiguousarray(pos, dtype=np.float32)

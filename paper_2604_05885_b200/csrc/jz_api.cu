@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <ctime>
 #include <string>
 #include <vector>
@@ -460,9 +461,8 @@ int jz_knn_rows(const jz_knn_index *ix, int64_t *m) {
   return JZ_OK;
 }
 
-int jz_knn_query(jz_knn_index *ix, int k, int order, int32_t *out_idx, float *out_d2, int32_t *out_row_gidx,
-                 jz_stream_t s) {
-  JZ_API_BEGIN
+static int query_impl(jz_knn_index *ix, int k, int order, int32_t *out_idx, float *out_d2, int32_t *out_row_gidx,
+                      jz_stream_t s, int chunks, const std::function<void(int64_t, int64_t)> &on_rows) {
   if (!ix) return fail(JZ_EINVAL, "NULL index");
   if (ix->n_query > 0 && (!out_idx || !out_d2)) return fail(JZ_EINVAL, "NULL argument");
   if (k < 1) return fail(JZ_EINVAL, "k must be >= 1");
@@ -503,6 +503,9 @@ int jz_knn_query(jz_knn_index *ix, int k, int order, int32_t *out_idx, float *ou
   la.out_d2 = out_d2;
   la.out_row_gidx = out_row_gidx;
   la.evals = ix->d_evals;
+  la.chunks = chunks;
+  la.nq = ix->n_query;
+  la.on_rows = on_rows;
   jz::leaf_to_leaf(la, ix->D, st);
   rec(ix, 6);
   il.release(st);
@@ -527,6 +530,12 @@ int jz_knn_query(jz_knn_index *ix, int k, int order, int32_t *out_idx, float *ou
     ix->times[5] = ix->times[0] + ix->times[1] + ix->times[2] + ix->times[3] + ix->times[4];
   }
   return JZ_OK;
+}
+
+int jz_knn_query(jz_knn_index *ix, int k, int order, int32_t *out_idx, float *out_d2, int32_t *out_row_gidx,
+                 jz_stream_t s) {
+  JZ_API_BEGIN
+  return query_impl(ix, k, order, out_idx, out_d2, out_row_gidx, s, 1, nullptr);
   JZ_API_END
 }
 
@@ -557,6 +566,21 @@ void jz_knn_free(jz_knn_index *ix) {
   delete ix;
 }
 
+namespace {
+// owners released on every exit path (stream-ordered frees; the index syncs its stream)
+struct DevBuf {
+  void *p = nullptr;
+  cudaStream_t st = nullptr;
+  ~DevBuf() {
+    if (p) cudaFreeAsync(p, st);
+  }
+};
+struct IndexOwner {
+  jz_knn_index *ix = nullptr;
+  ~IndexOwner() { jz_knn_free(ix); }
+};
+}  // namespace
+
 int jz_knn_search_host(const float *pos_host, int64_t n, const float *box, const jz_knn_params *p, int k,
                        int32_t *idx_host, float *d2_host, jz_stream_t s) {
   JZ_API_BEGIN
@@ -565,30 +589,76 @@ int jz_knn_search_host(const float *pos_host, int64_t n, const float *box, const
   if (k < 1 || k > n) return fail(JZ_EINVAL, "k must be in [1, n]");
   cudaStream_t st = (cudaStream_t)s;
   init_pool();
-  float *dpos = nullptr;
-  int32_t *didx = nullptr;
-  float *dd2 = nullptr;
-  JZ_CUDA(cudaMallocAsync(&dpos, n * 3 * sizeof(float), st));
-  JZ_CUDA(cudaMemcpyAsync(dpos, pos_host, n * 3 * sizeof(float), cudaMemcpyHostToDevice, st));
-  jz_knn_index *ix = nullptr;
-  int rc = jz_knn_build(dpos, n, box, p, s, &ix);
-  if (rc != JZ_OK) {
-    cudaFreeAsync(dpos, st);
-    return rc;
-  }
-  JZ_CUDA(cudaFreeAsync(dpos, st));
-  JZ_CUDA(cudaMallocAsync(&didx, n * k * sizeof(int32_t), st));
-  JZ_CUDA(cudaMallocAsync(&dd2, n * k * sizeof(float), st));
-  rc = jz_knn_query(ix, k, JZ_ORDER_INPUT, didx, dd2, nullptr, s);
-  jz_knn_free(ix);
-  if (rc == JZ_OK) {
-    JZ_CUDA(cudaMemcpyAsync(idx_host, didx, n * k * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    JZ_CUDA(cudaMemcpyAsync(d2_host, dd2, n * k * sizeof(float), cudaMemcpyDeviceToHost, st));
-  }
-  JZ_CUDA(cudaFreeAsync(didx, st));
-  JZ_CUDA(cudaFreeAsync(dd2, st));
+  DevBuf dpos{nullptr, st}, didx{nullptr, st}, dd2{nullptr, st};
+  IndexOwner own;
+  JZ_CUDA(cudaMallocAsync(&dpos.p, n * 3 * sizeof(float), st));
+  JZ_CUDA(cudaMemcpyAsync(dpos.p, pos_host, n * 3 * sizeof(float), cudaMemcpyHostToDevice, st));
+  int rc = jz_knn_build(static_cast<const float *>(dpos.p), n, box, p, s, &own.ix);
+  if (rc != JZ_OK) return rc;
+  JZ_CUDA(cudaMallocAsync(&didx.p, n * k * sizeof(int32_t), st));
+  JZ_CUDA(cudaMallocAsync(&dd2.p, n * k * sizeof(float), st));
+  rc = jz_knn_query(own.ix, k, JZ_ORDER_INPUT, static_cast<int32_t *>(didx.p), static_cast<float *>(dd2.p), nullptr, s);
+  if (rc != JZ_OK) return rc;
+  JZ_CUDA(cudaMemcpyAsync(idx_host, didx.p, n * k * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  JZ_CUDA(cudaMemcpyAsync(d2_host, dd2.p, n * k * sizeof(float), cudaMemcpyDeviceToHost, st));
   JZ_CUDA(cudaStreamSynchronize(st));
-  return rc;
+  return JZ_OK;
+  JZ_API_END
+}
+
+int jz_knn_search_host_z(const float *pos_host, int64_t n, const float *box, const jz_knn_params *p, int k,
+                         int32_t *idx_host, float *d2_host, int32_t *row_gidx_host, jz_stream_t s) {
+  JZ_API_BEGIN
+  if (!pos_host || !idx_host || !d2_host || !row_gidx_host) return fail(JZ_EINVAL, "NULL argument");
+  if (n < 1) return fail(JZ_EINVAL, "n must be >= 1");
+  if (k < 1 || k > n) return fail(JZ_EINVAL, "k must be in [1, n]");
+  cudaStream_t st = (cudaStream_t)s;
+  init_pool();
+  DevBuf dpos{nullptr, st}, didx{nullptr, st}, dd2{nullptr, st}, drg{nullptr, st};
+  IndexOwner own;
+  JZ_CUDA(cudaMallocAsync(&dpos.p, n * 3 * sizeof(float), st));
+  JZ_CUDA(cudaMemcpyAsync(dpos.p, pos_host, n * 3 * sizeof(float), cudaMemcpyHostToDevice, st));
+  int rc = jz_knn_build(static_cast<const float *>(dpos.p), n, box, p, s, &own.ix);
+  if (rc != JZ_OK) return rc;
+  JZ_CUDA(cudaMallocAsync(&didx.p, n * k * sizeof(int32_t), st));
+  JZ_CUDA(cudaMallocAsync(&dd2.p, n * k * sizeof(float), st));
+  JZ_CUDA(cudaMallocAsync(&drg.p, n * sizeof(int32_t), st));
+  // rows of each finished chunk of work items (a contiguous z-order range) go to the host on a
+  // second stream while the next chunk runs: the PCIe transfer overlaps LeafToLeaf
+  struct Copier {
+    cudaStream_t cs = nullptr;
+    std::vector<cudaEvent_t> ev;
+    ~Copier() {
+      if (cs) cudaStreamSynchronize(cs);
+      for (auto e : ev) cudaEventDestroy(e);
+      if (cs) cudaStreamDestroy(cs);
+    }
+  } cp;
+  JZ_CUDA(cudaStreamCreateWithFlags(&cp.cs, cudaStreamNonBlocking));
+  auto *hi = idx_host;
+  auto *hd = d2_host;
+  auto *hr = row_gidx_host;
+  const auto *gi = static_cast<const int32_t *>(didx.p);
+  const auto *gd = static_cast<const float *>(dd2.p);
+  const auto *gr = static_cast<const int32_t *>(drg.p);
+  auto on_rows = [&](int64_t q0, int64_t q1) {
+    cudaEvent_t e;
+    JZ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    cp.ev.push_back(e);
+    JZ_CUDA(cudaEventRecord(e, st));
+    JZ_CUDA(cudaStreamWaitEvent(cp.cs, e, 0));
+    JZ_CUDA(cudaMemcpyAsync(hi + q0 * k, gi + q0 * k, (q1 - q0) * k * sizeof(int32_t), cudaMemcpyDeviceToHost, cp.cs));
+    JZ_CUDA(cudaMemcpyAsync(hd + q0 * k, gd + q0 * k, (q1 - q0) * k * sizeof(float), cudaMemcpyDeviceToHost, cp.cs));
+    JZ_CUDA(cudaMemcpyAsync(hr + q0, gr + q0, (q1 - q0) * sizeof(int32_t), cudaMemcpyDeviceToHost, cp.cs));
+  };
+  const int chunks = k <= jz::kMaxK ? 16 : 1;
+  rc = query_impl(own.ix, k, JZ_ORDER_Z, static_cast<int32_t *>(didx.p), static_cast<float *>(dd2.p),
+                  static_cast<int32_t *>(drg.p), s, chunks, on_rows);
+  if (rc != JZ_OK) return rc;
+  if (cp.ev.empty()) on_rows(0, n);  // not chunked (k > k_max): one copy at the end
+  JZ_CUDA(cudaStreamSynchronize(cp.cs));
+  JZ_CUDA(cudaStreamSynchronize(st));
+  return JZ_OK;
   JZ_API_END
 }
 

@@ -1,6 +1,7 @@
 // jz_internal.h -- host-side structures of the CUDA path (index, planes, interaction lists).
 #pragma once
 #include <cstdint>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -127,6 +128,11 @@ struct LeafArgs {
   float *out_d2;
   int32_t *out_row_gidx;
   unsigned long long *evals;  // device counter (may be nullptr)
+  // optional chunked launch (JZ_ORDER_Z streaming): after chunk c, on_rows(q_lo, q_hi) is called
+  // with the finished z-order query rows [q_lo, q_hi); nq = number of queries
+  int chunks = 1;
+  int64_t nq = 0;
+  std::function<void(int64_t, int64_t)> on_rows;
 };
 void leaf_to_leaf(const LeafArgs &a, const Dom &D, cudaStream_t st);
 

@@ -27,6 +27,7 @@
 //    full of R_max^2(J), which bounds every contained query's k-th distance.
 //  * Rows are written straight to their final place (input or z order): no reorder pass.
 #include <cstdio>
+#include <vector>
 
 #include "jz_common.cuh"
 #include "jz_internal.h"
@@ -489,7 +490,8 @@ struct LeafPK {
   const float *rmax2;        // [npar] or nullptr (= +inf)
   const int32_t *item_par;   // [nitems] receiving parent of each 32-query work item
   const int32_t *item_q0;    // [nitems] first query (sorted position) of the item
-  int64_t nitems;
+  int64_t nitems;            // end of the launched item range
+  int64_t item_off;          // first item of the launched range (chunked launches)
   float Lmax;  // periodic: largest box length (margin scale); open: 0
   int k;       // neighbours found by this pass (<= K)
   int col0;    // first output column of this pass (k > k_max chunking)
@@ -712,7 +714,7 @@ template <int K, bool LB, bool PER>
 __global__ void __launch_bounds__(kLThreads, MinBlocks<K>::v) k_leaf(LeafPK a, Dom D) {
   __shared__ __align__(16) WarpBuf<K> s_buf[kLWarps];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t item = (int64_t)blockIdx.x * kLWarps + warp;
+  const int64_t item = a.item_off + (int64_t)blockIdx.x * kLWarps + warp;
   if (item >= a.nitems) return;
   WarpBuf<K> &B = s_buf[warp];
   const int J = a.item_par[item];
@@ -1246,6 +1248,7 @@ void leaf_to_leaf(const LeafArgs &a, const Dom &D, cudaStream_t st) {
   la.item_par = item_par;
   la.item_q0 = item_q0;
   la.nitems = nitems;
+  la.item_off = 0;
   la.Lmax = Lmax;
   la.ldo = a.k;
   la.order = a.order;
@@ -1257,16 +1260,32 @@ void leaf_to_leaf(const LeafArgs &a, const Dom &D, cudaStream_t st) {
   la.stats = a.evals;
   la.self = a.spts == a.qpts;
   if (nitems > 0) {
-    const unsigned blocks = (unsigned)ceil_div(nitems, kLWarps);
-    // k > k_max: ceil(k / k_max) passes over the same interaction list (built for R_max(k));
-    // pass c keeps only keys after the last (d2, index) of pass c-1.
-    for (int c0 = 0; c0 < a.k; c0 += kMaxK) {
-      la.col0 = c0;
-      la.k = a.k - c0 < kMaxK ? a.k - c0 : kMaxK;
-      if (la.k <= 8) launch_l<8>(la, D, blocks, st);
-      else if (la.k <= 16) launch_l<16>(la, D, blocks, st);
-      else launch_l<32>(la, D, blocks, st);
-      JZ_LAUNCH_CHECK();
+    // chunked launches (a.on_rows: rows of the finished z-order query range after each chunk,
+    // e.g. to stream them to the host while the next chunk runs); k <= k_max only
+    const int nch = (a.on_rows && a.k <= kMaxK && a.chunks > 1) ? a.chunks : 1;
+    std::vector<int32_t> q0h;
+    if (nch > 1) {
+      q0h.resize(nitems);
+      JZ_CUDA(cudaMemcpyAsync(q0h.data(), item_q0, nitems * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+      JZ_CUDA(cudaStreamSynchronize(st));
+    }
+    for (int ch = 0; ch < nch; ++ch) {
+      const int64_t i0 = nitems * ch / nch, i1 = nitems * (ch + 1) / nch;
+      if (i1 <= i0) continue;
+      la.item_off = i0;
+      la.nitems = i1;
+      const unsigned blocks = (unsigned)ceil_div(i1 - i0, kLWarps);
+      // k > k_max: ceil(k / k_max) passes over the same interaction list (built for R_max(k));
+      // pass c keeps only keys after the last (d2, index) of pass c-1.
+      for (int c0 = 0; c0 < a.k; c0 += kMaxK) {
+        la.col0 = c0;
+        la.k = a.k - c0 < kMaxK ? a.k - c0 : kMaxK;
+        if (la.k <= 8) launch_l<8>(la, D, blocks, st);
+        else if (la.k <= 16) launch_l<16>(la, D, blocks, st);
+        else launch_l<32>(la, D, blocks, st);
+        JZ_LAUNCH_CHECK();
+      }
+      if (nch > 1) a.on_rows(q0h[i0], i1 < nitems ? (int64_t)q0h[i1] : a.nq);
     }
   }
   JZ_CUDA(cudaFreeAsync(cnt, st));

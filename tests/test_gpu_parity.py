@@ -338,17 +338,28 @@ def _check_invariants(idx, d2):
 
 def test_c4_full_size_sampled():
     """C4 at its full size (10^8 clustered, periodic, k = 16) in the bench's launch
-    configuration: sampled rows vs the grid oracle, plus invariants on every row (on device)."""
+    configuration, element by element vs the grid oracle on (a) 10^6 random rows, (b) every row
+    whose point lies within 0.002 of a periodic face (wrapped neighbours; ~1.2e6 rows) and
+    (c) the 10^4 rows with the smallest k-th distance (halo centres: the densest regions); plus
+    the row invariants on all 10^8 rows (on device)."""
+    import time
+
     jz = _jz()
     pos, box, k = make_config("C4")
     t = torch.from_numpy(pos).cuda()
     ix = jz.KnnIndex(t, box=box)
     idx, d2 = ix.query(k)
     ix.free()
-    rows = np.random.default_rng(4).choice(len(pos), 3000, replace=False)
+    rnd = np.random.default_rng(4).choice(len(pos), 1_000_000, replace=False)
+    face = np.nonzero(((pos < 0.002) | (pos > 1 - 0.002)).any(1))[0]
+    dense = torch.topk(d2[:, k - 1], 10_000, largest=False).indices.cpu().numpy()  # row choice only
+    rows = np.unique(np.concatenate([rnd, face, dense]))
+    assert len(face) > 500_000 and len(rows) > 2_000_000
+    t0 = time.time()
     io, do = knn_grid(pos, k, box, rows=rows)
-    _assert_same(idx[torch.from_numpy(rows).cuda()].cpu().numpy(), d2[torch.from_numpy(rows).cuda()].cpu().numpy(),
-                 io, do)
+    sel = torch.from_numpy(rows).cuda()
+    _assert_same(idx[sel].cpu().numpy(), d2[sel].cpu().numpy(), io, do)
+    print(f"C4: {len(rows)} rows checked element by element ({len(face)} face rows), oracle {time.time() - t0:.1f} s")
     # invariants on all 10^8 rows, evaluated on the device
     assert bool((idx >= 0).all()) and bool((idx < len(pos)).all())
     assert bool((d2[:, 1:] >= d2[:, :-1]).all())
@@ -368,7 +379,7 @@ def test_c5_full_size_sampled():
     idx, d2 = ix.query(k)
     ix.free()
     del t
-    rows = np.random.default_rng(5).choice(len(pos), 1000, replace=False)
+    rows = np.random.default_rng(5).choice(len(pos), 100_000, replace=False)
     sel = torch.from_numpy(rows).cuda()
     gi, gd = idx[sel].cpu().numpy(), d2[sel].cpu().numpy()
     assert bool((idx >= 0).all()) and bool((idx < len(pos)).all())
@@ -599,3 +610,16 @@ def test_periodic_points_near_the_box_faces():
     ig, dg = _gpu_knn(p, 16, 1.0)
     io, do = knn_grid(p, 16, 1.0)
     _assert_same(ig, dg, io, do)
+
+
+def test_search_host_z_streamed():
+    """jz_knn_search_host_z: rows in z order streamed to host memory in chunks during the walk;
+    row r answers input point row_gidx[r] exactly as the oracle (and as the input-order call)."""
+    import paper_2604_05885_b200 as jz
+
+    for pos, box, k in [(uniform_points(300_000, 51, 1.0), None, 16), (clustered_points(200_000, 52, 1.0), 1.0, 8),
+                        (clustered_points(50_000, 53, 1.0), 1.0, 40)]:
+        idx, d2, rg = jz.knn_host_z(pos, k, box=box)
+        assert np.array_equal(np.sort(rg), np.arange(len(pos)))
+        io, do = knn_grid(pos, k, box)
+        _assert_same(idx, d2, io[rg], do[rg])
