@@ -329,6 +329,15 @@ JZ_API int jz_fof(jz_knn_index *ix, float r_link, int32_t min_count, int32_t *la
 JZ_API int jz_fof_catalogue(const jz_knn_index *ix, int64_t cap, int32_t *label, int32_t *count, double *com,
                             double *rad, jz_stream_t s);
 
+/* Group order of the last jz_fof: order [n] (device) = input rows in group order -- a
+ * stable sort of the points by their group's root, so the groups (all groups, singletons
+ * included) appear in z order of their roots and each group is a contiguous block internally in
+ * z order. group_beg [ngroups_all + 1] (device, optional, caller sizes it n + 1) = start of each
+ * block in order[], group_beg[ngroups_all] = n; *ngroups_all (host, optional). JZ_EINVAL before
+ * any jz_fof on this index. Synchronises s. */
+JZ_API int jz_fof_group_order(const jz_knn_index *ix, int32_t *order, int32_t *group_beg, int64_t *ngroups_all,
+                              jz_stream_t s);
+
 /* F2 -- multi-GPU rows in input order ("final reordering step": the
  * reverse all-to-all of the result). Step 1 (sender): the z-ordered rows of this rank
  * (idx [m][k] int32, d2 [m][k] float32, row_gidx [m] int32, from jz_knn_query with

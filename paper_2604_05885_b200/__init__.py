@@ -106,6 +106,17 @@ class KnnIndex:
                                                B.dptr(cat["com"]), B.dptr(cat["rad"]), st))
         return labels, cat
 
+    def fof_group_order(self):
+        """Group order of the last fof(): (order int32 [n] = input rows with every
+        group contiguous, groups in z order of their roots, z order inside; group_beg int32
+        [ngroups + 1] block starts)."""
+        order = torch.empty((self.n,), dtype=torch.int32, device=self.device)
+        beg = torch.empty((self.n + 1,), dtype=torch.int32, device=self.device)
+        ng = ctypes.c_int64()
+        B.check(self._lib.jz_fof_group_order(self._h, B.dptr(order), B.dptr(beg), ctypes.byref(ng),
+                                             B.stream_ptr(self.stream)))
+        return order, beg[: ng.value + 1]
+
     def stage_times(self):
         """Per-phase device ms of the last build + query (needs set_timing(True) before the build)."""
         t = (ctypes.c_float * 6)()

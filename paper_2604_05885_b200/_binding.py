@@ -25,7 +25,7 @@ EXPORTS = [
     "jz_fof", "jz_fof_catalogue",
     "jz_comm_unique_id", "jz_comm_init", "jz_comm_local_world", "jz_comm_init_local", "jz_comm_rank_size",
     "jz_comm_free", "jz_comm_world_free", "jz_knn_build_dist", "jz_knn_rows_dist", "jz_knn_query_dist",
-    "jz_knn_dist_stats", "jz_knn_search_host_z",
+    "jz_knn_dist_stats", "jz_knn_search_host_z", "jz_fof_group_order",
 ]
 
 
@@ -98,6 +98,7 @@ def lib():
             "jz_knn_query_dist": ([P, ctypes.c_int, ctypes.c_int, P, P, P, P], ctypes.c_int),
             "jz_knn_dist_stats": ([P, P, P], ctypes.c_int),
             "jz_knn_search_host_z": ([P, I64, P, P, ctypes.c_int, P, P, P, P], ctypes.c_int),
+            "jz_fof_group_order": ([P, P, P, P, P], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)

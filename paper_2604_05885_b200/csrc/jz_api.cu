@@ -557,6 +557,7 @@ void jz_knn_free(jz_knn_index *ix) {
   if (ix->perm) cudaFreeAsync(ix->perm, st);
   if (ix->d_evals) cudaFreeAsync(ix->d_evals, st);
   if (ix->fof_label) cudaFreeAsync(ix->fof_label, st);
+  if (ix->fof_root) cudaFreeAsync(ix->fof_root, st);
   if (ix->fof_count) cudaFreeAsync(ix->fof_count, st);
   if (ix->fof_com) cudaFreeAsync(ix->fof_com, st);
   if (ix->fof_rad) cudaFreeAsync(ix->fof_rad, st);
@@ -564,6 +565,26 @@ void jz_knn_free(jz_knn_index *ix) {
   for (auto &e : ix->ev)
     if (e) cudaEventDestroy(e);
   delete ix;
+}
+
+__global__ void k_iota_u32(uint32_t *__restrict__ a, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    a[i] = (uint32_t)i;
+}
+// group order: input id (.w) of the z position at each group-order slot
+__global__ void k_group_order_out(const float4 *__restrict__ pts, const uint32_t *__restrict__ zpos, int64_t n,
+                                  int32_t *__restrict__ order) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    order[i] = __float_as_int(pts[zpos[i]].w);
+}
+__global__ void k_group_heads(const uint32_t *__restrict__ root, int64_t n, int32_t *__restrict__ head) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    head[i] = (i == 0 || root[i] != root[i - 1]) ? 1 : 0;
+}
+__global__ void k_group_beg(const int32_t *__restrict__ head, const int64_t *__restrict__ off, int64_t n,
+                            int32_t *__restrict__ beg) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (head[i]) beg[off[i]] = (int32_t)i;
 }
 
 namespace {
@@ -677,8 +698,6 @@ int jz_fof(jz_knn_index *ix, float r_link, int32_t min_count, int32_t *labels, i
   jz::IList il;
   float *rmax2 = nullptr;
   int32_t *superbeg = nullptr;
-  jz::walk_to(ix->planes, ix->D, 1, ix->prm.ngr, ix->prm.flags, 1, il, &rmax2, &superbeg, st, b2);
-  rec(ix, 5);
   int32_t *par = nullptr, *minlab = nullptr, *cnt = nullptr, *flag = nullptr;
   double *sum = nullptr, *ss = nullptr;
   int64_t *pos = nullptr;
@@ -686,6 +705,10 @@ int jz_fof(jz_knn_index *ix, float r_link, int32_t min_count, int32_t *labels, i
   JZ_CUDA(cudaMallocAsync(&minlab, n * sizeof(int32_t), st));
   k_fof_init<<<jz::grid_for(n, 256), 256, 0, st>>>(par, minlab, n);
   JZ_LAUNCH_CHECK();
+  // node-level walk: ParentToNode, three-case NodeToNode with node links; linked
+  // leaves' points start in their group (par), the remaining pairs go to the leaf stage
+  jz::fof_walk(ix->planes, ix->D, ix->prm.ngr, b2, il, &superbeg, par, n, st);
+  rec(ix, 5);
   if (!ix->d_evals) JZ_CUDA(cudaMallocAsync(&ix->d_evals, 16 * sizeof(unsigned long long), st));
   JZ_CUDA(cudaMemsetAsync(ix->d_evals, 0, 16 * sizeof(unsigned long long), st));
   const bool one_plane = ix->planes.size() == 1;
@@ -744,8 +767,10 @@ int jz_fof(jz_knn_index *ix, float r_link, int32_t min_count, int32_t *labels, i
   il.release(st);
   if (rmax2) JZ_CUDA(cudaFreeAsync(rmax2, st));
   if (superbeg) JZ_CUDA(cudaFreeAsync(superbeg, st));
-  for (void *p : {(void *)par, (void *)minlab, (void *)cnt, (void *)sum, (void *)ss, (void *)flag, (void *)pos})
+  for (void *p : {(void *)minlab, (void *)cnt, (void *)sum, (void *)ss, (void *)flag, (void *)pos})
     JZ_CUDA(cudaFreeAsync(p, st));
+  if (ix->fof_root) JZ_CUDA(cudaFreeAsync(ix->fof_root, st));
+  ix->fof_root = par;  // roots (flattened) kept for jz_fof_group_order
   unsigned long long ev = 0;
   JZ_CUDA(cudaMemcpyAsync(&ev, ix->d_evals, sizeof(ev), cudaMemcpyDeviceToHost, st));
   JZ_CUDA(cudaStreamSynchronize(st));
@@ -774,6 +799,47 @@ int jz_fof_catalogue(const jz_knn_index *ix, int64_t cap, int32_t *label, int32_
     JZ_CUDA(cudaMemcpyAsync(com, ix->fof_com, 3 * ng * sizeof(double), cudaMemcpyDeviceToDevice, st));
     JZ_CUDA(cudaMemcpyAsync(rad, ix->fof_rad, ng * sizeof(double), cudaMemcpyDeviceToDevice, st));
   }
+  return JZ_OK;
+  JZ_API_END
+}
+
+int jz_fof_group_order(const jz_knn_index *ix, int32_t *order, int32_t *group_beg, int64_t *ngroups_all,
+                       jz_stream_t s) {
+  JZ_API_BEGIN
+  if (!ix || !order) return fail(JZ_EINVAL, "NULL argument");
+  if (!ix->fof_root) return fail(JZ_EINVAL, "no friends-of-friends result in this index (call jz_fof first)");
+  cudaStream_t st = (cudaStream_t)s;
+  const int64_t n = ix->n;
+  // stable sort of the z positions by their root z position: roots stay in z order and
+  // every group is a contiguous block, internally in z order
+  DevBuf iota{nullptr, st}, skey{nullptr, st}, sval{nullptr, st}, flag{nullptr, st}, off{nullptr, st};
+  JZ_CUDA(cudaMallocAsync(&iota.p, n * sizeof(uint32_t), st));
+  JZ_CUDA(cudaMallocAsync(&skey.p, n * sizeof(uint32_t), st));
+  JZ_CUDA(cudaMallocAsync(&sval.p, n * sizeof(uint32_t), st));
+  k_iota_u32<<<jz::grid_for(n, 256), 256, 0, st>>>(static_cast<uint32_t *>(iota.p), n);
+  JZ_LAUNCH_CHECK();
+  jz::sort_pairs_u32(reinterpret_cast<const uint32_t *>(ix->fof_root), static_cast<const uint32_t *>(iota.p), n,
+                     static_cast<uint32_t *>(skey.p), static_cast<uint32_t *>(sval.p), st);
+  k_group_order_out<<<jz::grid_for(n, 256), 256, 0, st>>>(ix->pts, static_cast<const uint32_t *>(sval.p), n, order);
+  JZ_LAUNCH_CHECK();
+  if (group_beg || ngroups_all) {  // group starts: positions where the root changes
+    JZ_CUDA(cudaMallocAsync(&flag.p, n * sizeof(int32_t), st));
+    JZ_CUDA(cudaMallocAsync(&off.p, (n + 1) * sizeof(int64_t), st));
+    k_group_heads<<<jz::grid_for(n, 256), 256, 0, st>>>(static_cast<const uint32_t *>(skey.p), n,
+                                                        static_cast<int32_t *>(flag.p));
+    JZ_LAUNCH_CHECK();
+    jz::exclusive_scan_i32_to_i64(static_cast<int32_t *>(flag.p), static_cast<int64_t *>(off.p), n, st);
+    const int64_t ng = jz::read_i64(static_cast<int64_t *>(off.p) + n, st);
+    if (group_beg) {
+      k_group_beg<<<jz::grid_for(n, 256), 256, 0, st>>>(static_cast<const int32_t *>(flag.p),
+                                                        static_cast<const int64_t *>(off.p), n, group_beg);
+      JZ_LAUNCH_CHECK();
+      const int32_t nn = (int32_t)n;
+      JZ_CUDA(cudaMemcpyAsync(group_beg + ng, &nn, sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    }
+    if (ngroups_all) *ngroups_all = ng;
+  }
+  JZ_CUDA(cudaStreamSynchronize(st));
   return JZ_OK;
   JZ_API_END
 }

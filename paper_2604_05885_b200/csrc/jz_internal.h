@@ -59,6 +59,7 @@ struct jz_knn_index {
   int64_t fof_ngroups = 0;
   int32_t *fof_label = nullptr, *fof_count = nullptr;
   double *fof_com = nullptr, *fof_rad = nullptr;
+  int32_t *fof_root = nullptr;  // [n] root z position of each z position (last jz_fof; group order)
   // multi-GPU (jz_knn_build_dist): this rank's part of a distributed index (jz_dist.cu)
   jz_comm *comm = nullptr;
   int64_t n_own = 0, gidx_base = 0;  // this rank's input slice: global ids [gidx_base, gidx_base + n_own)
@@ -78,6 +79,9 @@ void compute_frame(const float *pos, int64_t n, int stride, const Dom &D, const 
 void sort_points(const float *pos, int64_t n, int stride, int gidx_mode, int64_t gidx_base, const Frame &frame,
                  uint64_t *keys_out, int32_t *perm_out, float4 *pts_out, cudaStream_t st);
 void morton_keys(const float *pos, int64_t n, const Frame &f, uint64_t *keys, cudaStream_t st);
+// stable LSD sort of 32-bit (key, value) pairs (one-sweep passes; in and out buffers distinct)
+void sort_pairs_u32(const uint32_t *keys, const uint32_t *vals, int64_t n, uint32_t *keys_out, uint32_t *vals_out,
+                    cudaStream_t st);
 void local_bbox(const float *pos, int64_t n, int stride, const Dom &D, float lo[3], float hi[3], cudaStream_t st);
 
 // tree (jz_build.cu)
@@ -106,6 +110,12 @@ struct IList {
 void walk_to(const std::vector<Plane> &planes, const Dom &D, int k, int ngr, unsigned flags, int stop, IList &il,
              float **rmax2, int32_t **superbeg, cudaStream_t st, float fixed_r2 = -1.f,
              const int32_t *qbeg = nullptr);
+
+// friends-of-friends walk with node links (§5): lists of plane-1 receivers
+// (pairs of nodes neither too far nor fully linked) and the point-level union-find start par[npts]
+// (points of linked leaves point to the first point of their group's root leaf)
+void fof_walk(const std::vector<Plane> &planes, const Dom &D, int ngr, float b2, IList &out_il,
+              int32_t **superbeg_out, int32_t *par, int64_t npts, cudaStream_t st);
 
 // leaf-to-leaf (jz_leaf.cu)
 struct LeafArgs {

@@ -55,6 +55,10 @@ static_assert(JZ_LCAP >= kMaxLeaf, "a leaf must fit the staging buffer");
 #define JZ_STATS 0  // per-lane walk counters (appends, merge rounds, compactions): diagnostic builds (tools/mkvar.py)
 #endif
 
+#ifndef JZ_FOF_FULL
+#define JZ_FOF_FULL 0  // 1: link whole (item, leaf) pairs within R_link without evaluating them (measured slower at 10^8 C4: 104 vs 89 ms)
+#endif
+
 #ifndef JZ_MERGE_T
 #define JZ_MERGE_T 0  // > 0: merge at a batch end only when some lane has >= JZ_MERGE_T new log entries
 #endif
@@ -942,6 +946,7 @@ struct FofPK {
   const float4 *spts;
   const int32_t *sbeg;
   const CE *leaf_ce;
+  const NodeBox *leaf_box;  // exact boxes: d_up test of a whole (item, leaf) pair
   const int32_t *par_leaf;
   const CE *par_ce;
   const int64_t *ispl;
@@ -1041,6 +1046,11 @@ __global__ void __launch_bounds__(kLThreads, 12) k_fof_leaf(FofPK a, Dom D) {
     }
   }
   const CE wb = make_ce(blo[0], blo[1], blo[2], bhi[0], bhi[1], bhi[2], a.Lmax);
+  NodeBox wnb;  // the item's query box (exact bounds for the d_up test)
+  wnb.lo = make_float4(blo[0], blo[1], blo[2], 0.f);
+  wnb.hi = make_float4(bhi[0], bhi[1], bhi[2], 0.f);
+  // a whole (item, leaf) pair can only be within R_link if the item box is (d_up >= diag / 2)
+  const bool small = JZ_FOF_FULL && __fmul_rd(box_dup2(wnb, wnb, D), 0.25f) <= a.b2;
   const float b2 = a.b2;
   unsigned long long nev = 0;
   // own leaves [xa, xb): their sources are contiguous; every pair inside is a candidate
@@ -1101,7 +1111,7 @@ __global__ void __launch_bounds__(kLThreads, 12) k_fof_leaf(FofPK a, Dom D) {
     const int ya = S == J ? xa : 0, yb = S == J ? xb : 0;
     for (int l0 = la; l0 < lb; l0 += 32) {
       const int l = l0 + lane;
-      bool pass = false;
+      bool pass = false, full = false;
       int cls = 0, s0 = 0, s1 = 0;
       float cx = 0.f, cy = 0.f, cz = 0.f, ex = 0.f, ey = 0.f, ez = 0.f;
       if (l < lb && (l < ya || l >= yb)) {
@@ -1119,8 +1129,18 @@ __global__ void __launch_bounds__(kLThreads, 12) k_fof_leaf(FofPK a, Dom D) {
         pass = s1 > q0 + 1 && dlow2_ce<PER>(dcx, dcy, dcz, Ex, Ey, Ez, D) <= b2;  // a source after some query
         if (PER && pass)
           cls = ce_class(dcx, Ex, D.h[0]) | (ce_class(dcy, Ey, D.h[1]) << 2) | (ce_class(dcz, Ez, D.h[2]) << 4);
+        // every (query, source) pair of the item and the leaf within R_link (P:L486 case 2 at the
+        // leaf level): link all of them through the leaf's first point instead of evaluating pairs
+        full = small && pass && box_dup2(wnb, a.leaf_box[l], D) <= b2;
       }
-      unsigned bal = __ballot_sync(0xffffffffu, pass);
+      const unsigned fb = __ballot_sync(0xffffffffu, full);
+      for (unsigned f = fb; f; f &= f - 1) {
+        const int src = __ffs(f) - 1;
+        const int lp = __shfl_sync(0xffffffffu, s0, src), le = __shfl_sync(0xffffffffu, s1, src);
+        if (act) fof_union(a.par, qi, lp);
+        for (int t = lp + 1 + lane; t < le; t += 32) fof_union(a.par, t, lp);
+      }
+      unsigned bal = __ballot_sync(0xffffffffu, pass && !full);
       while (bal) {
         const int c0 = __shfl_sync(0xffffffffu, cls, __ffs(bal) - 1);
         int n = 0;
@@ -1338,6 +1358,7 @@ void fof_leaf(const LeafArgs &a, const Dom &D, float b2, int32_t *par, cudaStrea
   f.spts = a.spts;
   f.sbeg = a.sbeg;
   f.leaf_ce = leaf_ce;
+  f.leaf_box = a.leaf_box;
   f.par_leaf = a.par_leaf;
   f.par_ce = par_ce;
   f.ispl = a.il->ispl;

@@ -796,6 +796,82 @@ void sort_points(const float *pos, int64_t n, int stride, int gidx_mode, int64_t
   if (fb) sort_points8(pos, n, stride, gidx_mode, gidx_base, frame, keys_out, perm_out, pts_out, st);
 }
 
+// ---------------------------------------------------------------- stable sort of 32-bit (key, value) pairs
+// (friends-of-friends group order): the one-sweep passes above over the key bytes
+__global__ void __launch_bounds__(256) k_hist_u32(const uint32_t *__restrict__ k, int64_t n,
+                                                  unsigned int *__restrict__ hist /*[4][256]*/) {
+  __shared__ unsigned int s_h[4][kRadix];
+  for (int i = threadIdx.x; i < 4 * kRadix; i += blockDim.x) (&s_h[0][0])[i] = 0;
+  __syncthreads();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t v = k[i];
+#pragma unroll
+    for (int ps = 0; ps < 4; ++ps) atomicAdd(&s_h[ps][(v >> (8 * ps)) & 255], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 4 * kRadix; i += blockDim.x) {
+    const unsigned v = (&s_h[0][0])[i];
+    if (v) atomicAdd(&hist[i], v);
+  }
+}
+
+void sort_pairs_u32(const uint32_t *keys, const uint32_t *vals, int64_t n, uint32_t *keys_out, uint32_t *vals_out,
+                    cudaStream_t st) {
+  if (n <= 0) return;
+  unsigned int *dhist = nullptr;
+  JZ_CUDA(cudaMallocAsync(&dhist, 4 * kRadix * sizeof(unsigned), st));
+  JZ_CUDA(cudaMemsetAsync(dhist, 0, 4 * kRadix * sizeof(unsigned), st));
+  k_hist_u32<<<grid_for(n, 256, 148 * 4), 256, 0, st>>>(keys, n, dhist);
+  JZ_LAUNCH_CHECK();
+  std::vector<unsigned> hist(4 * kRadix), bases(4 * kRadix);
+  JZ_CUDA(cudaMemcpyAsync(hist.data(), dhist, hist.size() * sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+  JZ_CUDA(cudaStreamSynchronize(st));
+  std::vector<int> passes;
+  for (int p = 0; p < 4; ++p) {
+    unsigned acc = 0;
+    bool trivial = false;
+    for (int b = 0; b < kRadix; ++b) {
+      bases[p * kRadix + b] = acc;
+      if (hist[p * kRadix + b] == (unsigned)n) trivial = true;
+      acc += hist[p * kRadix + b];
+    }
+    if (!trivial) passes.push_back(p);
+  }
+  JZ_CUDA(cudaMemcpyAsync(dhist, bases.data(), bases.size() * sizeof(unsigned), cudaMemcpyHostToDevice, st));
+  const int64_t ntiles = ceil_div(n, kS32Tile);
+  unsigned long long *status = nullptr;
+  int *counters = nullptr;
+  uint32_t *tk = nullptr, *tv = nullptr;
+  JZ_CUDA(cudaMallocAsync(&status, (size_t)ntiles * kRadix * sizeof(unsigned long long), st));
+  JZ_CUDA(cudaMallocAsync(&counters, 4 * sizeof(int), st));
+  JZ_CUDA(cudaMemsetAsync(counters, 0, 4 * sizeof(int), st));
+  JZ_CUDA(cudaMallocAsync(&tk, n * sizeof(uint32_t), st));
+  JZ_CUDA(cudaMallocAsync(&tv, n * sizeof(uint32_t), st));
+  const uint32_t *ki = keys, *vi = vals;
+  const int np = (int)passes.size();
+  for (int i = 0; i < np; ++i) {
+    // ping-pong so that the last pass lands in keys_out / vals_out
+    const bool to_out = ((np - 1 - i) & 1) == 0;
+    uint32_t *ko = to_out ? keys_out : tk, *vo = to_out ? vals_out : tv;
+    JZ_CUDA(cudaMemsetAsync(status, 0, (size_t)ntiles * kRadix * sizeof(unsigned long long), st));
+    k_onesweep32<false, false><<<(unsigned)ntiles, kS32Threads, 0, st>>>(nullptr, 0, 0, 0, Frame{}, ki, vi, ko, vo,
+                                                                          nullptr, nullptr, n, 8 * passes[i], 0,
+                                                                          dhist + passes[i] * kRadix, status, counters + i);
+    JZ_LAUNCH_CHECK();
+    ki = ko;
+    vi = vo;
+  }
+  if (np == 0) {  // already sorted (one key value)
+    JZ_CUDA(cudaMemcpyAsync(keys_out, keys, n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
+    JZ_CUDA(cudaMemcpyAsync(vals_out, vals, n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
+  }
+  JZ_CUDA(cudaFreeAsync(status, st));
+  JZ_CUDA(cudaFreeAsync(counters, st));
+  JZ_CUDA(cudaFreeAsync(tk, st));
+  JZ_CUDA(cudaFreeAsync(tv, st));
+  JZ_CUDA(cudaFreeAsync(dhist, st));
+}
+
 // Morton keys only (multi-GPU splitter step)
 __global__ void k_keys(const float *__restrict__ pos, int64_t n, Frame f, uint64_t *__restrict__ keys) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)

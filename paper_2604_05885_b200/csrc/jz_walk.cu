@@ -14,6 +14,7 @@
 //   k_segsort     sort each receiver's segment by (rlow, isrc) (P:L396 bitonic network).
 // All bounds are squared FP32 values that bound the canonical d2 exactly (jz_common.cuh).
 #include <climits>
+#include <cstring>
 #include <vector>
 
 #include "jz_common.cuh"
@@ -355,6 +356,281 @@ void walk_to(const std::vector<Plane> &planes, const Dom &D, int k, int ngr, uns
     JZ_CUDA(cudaFreeAsync(superbeg, st));
     *superbeg_out = nullptr;
   }
+}
+
+
+// ---------------------------------------------------------------- friends-of-friends walk (F4)
+// PAPER.md §5 "Implementation" (L477-490): a group pointer per node is carried down the planes.
+// ParentToNode: a node whose parent's group is linked points to the first child of that group's
+// root, else to itself; a node is (self-)linked if its group is linked or its diagonal
+// is <= R_link (d_up(A, A)^2 <= b2). NodeToNode distinguishes three cases:
+// (1) same linked group or d_low^2 > b2: discarded; (2) d_up^2 <= b2: the two nodes are linked
+// (union of their groups, lower root wins, CAS + retry); (3) otherwise the pair goes to
+// the list of the next plane. After the links the pointers are contracted to their roots.
+// Bounds are the exact monotone box bounds of jz_common.cuh (R8): d_up^2 <= b2 means every point
+// pair of the two nodes has canonical d2 <= b2.
+__device__ __forceinline__ int gfind(int32_t *g, int x) {
+  while (true) {
+    const int p = __ldcg(&g[x]);
+    if (p == x) return x;
+    const int pp = __ldcg(&g[p]);
+    if (pp == p) return p;
+    __stcg(&g[x], pp);  // path halving: pp is an ancestor of x (benign race)
+    x = pp;
+  }
+}
+
+__device__ __forceinline__ void gunion(int32_t *g, int a, int b) {
+  while (true) {
+    a = gfind(g, a);
+    b = gfind(g, b);
+    if (a == b) return;
+    if (a > b) {
+      const int t = a;
+      a = b;
+      b = t;
+    }
+    const int old = atomicCAS(&g[b], b, a);
+    if (old == b) return;
+    b = old;
+  }
+}
+
+// top plane (no linked parent): own pointer, self-linked iff the diagonal is <= R_link
+__global__ void k_fof_top(const NodeBox *__restrict__ box, int64_t n, Dom D, float b2, int32_t *__restrict__ g,
+                          uint8_t *__restrict__ lk) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const NodeBox b = box[i];
+    g[i] = (int32_t)i;
+    lk[i] = box_dup2(b, b, D) <= b2;
+  }
+}
+
+// ParentToNode: children of parent P (plane p+1, child ranges pbeg) on plane p
+__global__ void k_fof_p2n(const int32_t *__restrict__ pbeg, int64_t npar, const int32_t *__restrict__ gp,
+                          const uint8_t *__restrict__ lkp, const NodeBox *__restrict__ box, Dom D, float b2,
+                          int32_t *__restrict__ g, uint8_t *__restrict__ lk) {
+  for (int64_t P = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; P < npar; P += (int64_t)gridDim.x * blockDim.x) {
+    const bool linked = lkp[P];
+    const int first = linked ? pbeg[gp[P]] : 0;  // first child of the root of the parent's group
+    for (int c = pbeg[P]; c < pbeg[P + 1]; ++c) {
+      const NodeBox b = box[c];
+      g[c] = linked ? first : c;
+      lk[c] = linked || box_dup2(b, b, D) <= b2;
+    }
+  }
+}
+
+// smallest quarter squared diagonal of the plane's nodes (float bits, atomicMin): a pair (c, s) can
+// only be fully linked if d_up(c, s)^2 <= b2, and d_up(c, s) >= max(diag c, diag s) / 2
+__global__ void k_fof_mindiag(const NodeBox *__restrict__ box, int64_t n, Dom D, unsigned *__restrict__ out) {
+  unsigned m = 0x7f800000u;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const NodeBox b = box[i];
+    m = min(m, __float_as_uint(__fmul_rd(box_dup2(b, b, D), 0.25f)));
+  }
+  m = __reduce_min_sync(0xffffffffu, m);
+  if ((threadIdx.x & 31) == 0) atomicMin(out, m);
+}
+
+__global__ void k_fof_contract(int32_t *__restrict__ g, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    g[i] = gfind(g, (int)i);
+}
+
+enum { FLINK = 0, FCOUNT = 1, FINSERT = 2 };
+
+// one warp per receiving parent J, one lane per child c; source children of every entry of J's list
+// staged in shared memory (as k_n2n); MODE FLINK: case (2) links; FCOUNT / FINSERT: case (3) pairs
+template <int MODE, bool LINKS>
+__global__ void __launch_bounds__(kN2NWarps * 32) k_fof_n2n(const int32_t *__restrict__ pbeg, int64_t npar,
+                                                           const int64_t *__restrict__ ispl,
+                                                           const int32_t *__restrict__ isrc,
+                                                           const NodeBox *__restrict__ cbox, Dom D, float b2,
+                                                           int32_t *__restrict__ g, uint8_t *__restrict__ lk,
+                                                           int32_t *__restrict__ cnt,
+                                                           const int64_t *__restrict__ ispl_out,
+                                                           int32_t *__restrict__ isrc_out, float *__restrict__ rlow_out) {
+  __shared__ NodeBox s_box[kN2NWarps][kN2NWStage];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t J = (int64_t)blockIdx.x * kN2NWarps + warp;
+  if (J >= npar) return;
+  NodeBox *sb = s_box[warp];
+  const int cb = pbeg[J], ce = pbeg[J + 1];
+  const int64_t eb = ispl[J], ee = ispl[J + 1];
+  for (int c0 = cb; c0 < ce; c0 += 32) {
+    const int c = c0 + lane;
+    const bool valid = c < ce;
+    NodeBox mb;
+    int rc = 0;
+    bool lc = false;
+    if (valid) {
+      mb = cbox[c];
+      if (MODE != FLINK) {
+        rc = g[c];  // contracted
+        lc = lk[c];
+      }
+    }
+    int count = 0;
+    int64_t wp = (MODE == FINSERT && valid) ? ispl_out[c] : 0;
+    for (int64_t e = eb; e < ee; ++e) {
+      const int S = isrc[e];
+      const int sb0 = pbeg[S], se = pbeg[S + 1];
+      for (int s0 = sb0; s0 < se; s0 += kN2NWStage) {
+        const int sn = min(kN2NWStage, se - s0);
+        __syncwarp();
+        for (int t = lane; t < sn; t += 32) sb[t] = cbox[s0 + t];
+        __syncwarp();
+        if (valid) {
+          for (int t = 0; t < sn; ++t) {
+            const int s = s0 + t;
+            const NodeBox sbx = sb[t];
+            const float dl = box_dlow2(mb, sbx, D);
+            if (dl > b2) continue;                                   // case (1): too far
+            const bool full = LINKS && box_dup2(mb, sbx, D) <= b2;  // case (2): every pair within R_link
+            if (MODE == FLINK) {
+              if (full && s != c) {
+                gunion(g, c, s);
+                lk[c] = 1;
+                lk[s] = 1;
+              }
+            } else {
+              if (full) continue;
+              if (LINKS && lc && g[s] == rc) continue;  // case (1): same linked group
+              if (MODE == FCOUNT) ++count;
+              else {
+                isrc_out[wp] = s;
+                rlow_out[wp] = dl;
+                ++wp;
+              }
+            }
+          }
+        }
+      }
+    }
+    if (valid && MODE == FCOUNT) cnt[c] = count;
+  }
+}
+
+__global__ void k_fof_point_init(const int32_t *__restrict__ beg, int64_t nleaf, const int32_t *__restrict__ g,
+                                 const uint8_t *__restrict__ lk, int32_t *__restrict__ par) {
+  for (int64_t l = blockIdx.x; l < nleaf; l += gridDim.x) {
+    const bool linked = lk[l];
+    const int first = linked ? beg[g[l]] : 0;
+    for (int x = beg[l] + threadIdx.x; x < beg[l + 1]; x += blockDim.x) par[x] = linked ? first : x;
+  }
+}
+
+// the walk of friends-of-friends down to plane 1 (receivers of the leaf stage) with node links;
+// writes the point-level union-find initialisation: par[x] = first point of the root leaf of x's
+// group when x's leaf is linked (all its points are in that component), else x
+void fof_walk(const std::vector<Plane> &planes, const Dom &D, int ngr, float b2, IList &out_il,
+              int32_t **superbeg_out, int32_t *par, int64_t npts, cudaStream_t st) {
+  const int P = (int)planes.size();
+  const int top = P - 1;
+  if (P < 2) {  // one plane: the dense super-node list, no node links (par stays the identity)
+    float *rmax2 = nullptr;
+    walk_to(planes, D, 1, ngr, 0, 1, out_il, &rmax2, superbeg_out, st, b2);
+    if (rmax2) JZ_CUDA(cudaFreeAsync(rmax2, st));
+    return;
+  }
+  const int64_t ntop = planes[top].nnodes;
+  const int64_t S = ceil_div(ntop, ngr);
+  int32_t *superbeg = nullptr;
+  JZ_CUDA(cudaMallocAsync(&superbeg, (S + 1) * sizeof(int32_t), st));
+  k_super_beg<<<grid_for(S + 1, 256), 256, 0, st>>>(S, ntop, ngr, superbeg);
+  JZ_LAUNCH_CHECK();
+  IList il;
+  il.nrecv = S;
+  il.total = S * S;
+  JZ_CUDA(cudaMallocAsync(&il.ispl, (S + 1) * sizeof(int64_t), st));
+  JZ_CUDA(cudaMallocAsync(&il.isrc, il.total * sizeof(int32_t), st));
+  JZ_CUDA(cudaMallocAsync(&il.rlow, il.total * sizeof(float), st));
+  k_dense_init<<<grid_for(S * S + 2, 256), 256, 0, st>>>(S, il.ispl, il.isrc, il.rlow);
+  JZ_LAUNCH_CHECK();
+  int32_t *gp = nullptr;
+  uint8_t *lkp = nullptr;
+  unsigned *mind = nullptr;
+  JZ_CUDA(cudaMallocAsync(&mind, sizeof(unsigned), st));
+  for (int p = top; p >= 0; --p) {
+    const Plane &pl = planes[p];
+    int32_t *g = nullptr;
+    uint8_t *lk = nullptr;
+    JZ_CUDA(cudaMallocAsync(&g, (pl.nnodes > 0 ? pl.nnodes : 1) * sizeof(int32_t), st));
+    JZ_CUDA(cudaMallocAsync(&lk, pl.nnodes > 0 ? pl.nnodes : 1, st));
+    if (p == top) {
+      k_fof_top<<<grid_for(pl.nnodes, 256), 256, 0, st>>>(pl.box, pl.nnodes, D, b2, g, lk);
+    } else {
+      k_fof_p2n<<<grid_for(planes[p + 1].nnodes, 256), 256, 0, st>>>(planes[p + 1].beg, planes[p + 1].nnodes, gp, lkp,
+                                                                      pl.box, D, b2, g, lk);
+    }
+    JZ_LAUNCH_CHECK();
+    if (gp) JZ_CUDA(cudaFreeAsync(gp, st));
+    if (lkp) JZ_CUDA(cudaFreeAsync(lkp, st));
+    gp = g;
+    lkp = lk;
+    if (p == 0) break;  // leaves: pairs are the leaf stage's (plane-1 lists)
+    const int32_t *pbeg = (p == top) ? superbeg : planes[p + 1].beg;
+    const int64_t npar = (p == top) ? S : planes[p + 1].nnodes;
+    const unsigned blocks = (unsigned)ceil_div(npar, kN2NWarps);
+    // node links are only possible if some node of the plane is small enough (quarter squared
+    // diagonal <= b2); otherwise the plane is walked with the plain fixed-radius test
+    JZ_CUDA(cudaMemsetAsync(mind, 0x7f, sizeof(unsigned), st));
+    k_fof_mindiag<<<grid_for(pl.nnodes, 256, 148 * 4), 256, 0, st>>>(pl.box, pl.nnodes, D, mind);
+    JZ_LAUNCH_CHECK();
+    unsigned mh = 0;
+    JZ_CUDA(cudaMemcpyAsync(&mh, mind, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    JZ_CUDA(cudaStreamSynchronize(st));
+    float mdq;
+    memcpy(&mdq, &mh, 4);
+    const bool links = mdq <= b2;
+    if (links) {
+      k_fof_n2n<FLINK, true><<<blocks, kN2NWarps * 32, 0, st>>>(pbeg, npar, il.ispl, il.isrc, pl.box, D, b2, g, lk,
+                                                                 nullptr, nullptr, nullptr, nullptr);
+      JZ_LAUNCH_CHECK();
+      k_fof_contract<<<grid_for(pl.nnodes, 256), 256, 0, st>>>(g, pl.nnodes);
+      JZ_LAUNCH_CHECK();
+    }
+    int32_t *cnt = nullptr;
+    JZ_CUDA(cudaMallocAsync(&cnt, pl.nnodes * sizeof(int32_t), st));
+    if (links)
+      k_fof_n2n<FCOUNT, true><<<blocks, kN2NWarps * 32, 0, st>>>(pbeg, npar, il.ispl, il.isrc, pl.box, D, b2, g, lk, cnt,
+                                                                  nullptr, nullptr, nullptr);
+    else
+      k_fof_n2n<FCOUNT, false><<<blocks, kN2NWarps * 32, 0, st>>>(pbeg, npar, il.ispl, il.isrc, pl.box, D, b2, g, lk,
+                                                                   cnt, nullptr, nullptr, nullptr);
+    JZ_LAUNCH_CHECK();
+    IList nl;
+    nl.nrecv = pl.nnodes;
+    JZ_CUDA(cudaMallocAsync(&nl.ispl, (pl.nnodes + 1) * sizeof(int64_t), st));
+    exclusive_scan_i32_to_i64(cnt, nl.ispl, pl.nnodes, st);
+    nl.total = read_i64(nl.ispl + pl.nnodes, st);
+    JZ_CUDA(cudaMallocAsync(&nl.isrc, (nl.total > 0 ? nl.total : 1) * sizeof(int32_t), st));
+    JZ_CUDA(cudaMallocAsync(&nl.rlow, (nl.total > 0 ? nl.total : 1) * sizeof(float), st));
+    if (links)
+      k_fof_n2n<FINSERT, true><<<blocks, kN2NWarps * 32, 0, st>>>(pbeg, npar, il.ispl, il.isrc, pl.box, D, b2, g, lk,
+                                                                   nullptr, nl.ispl, nl.isrc, nl.rlow);
+    else
+      k_fof_n2n<FINSERT, false><<<blocks, kN2NWarps * 32, 0, st>>>(pbeg, npar, il.ispl, il.isrc, pl.box, D, b2, g, lk,
+                                                                    nullptr, nl.ispl, nl.isrc, nl.rlow);
+    JZ_LAUNCH_CHECK();
+    // segments in (d_low, source) order, as the kNN walk: nearby source nodes first
+    k_segsort<<<grid_for(pl.nnodes, kSegWarps, 148 * 16), kSegWarps * 32, 0, st>>>(nl.ispl, nl.nrecv, nl.isrc, nl.rlow);
+    JZ_LAUNCH_CHECK();
+    il.release(st);
+    il = nl;
+    JZ_CUDA(cudaFreeAsync(cnt, st));
+    if (p == 1) out_il = il;
+  }
+  // gp / lkp: leaf groups (ParentToNode from plane 1) -> point-level initialisation
+  k_fof_point_init<<<grid_for(planes[0].nnodes, 128), 128, 0, st>>>(planes[0].beg, planes[0].nnodes, gp, lkp, par);
+  JZ_LAUNCH_CHECK();
+  JZ_CUDA(cudaFreeAsync(gp, st));
+  JZ_CUDA(cudaFreeAsync(lkp, st));
+  JZ_CUDA(cudaFreeAsync(mind, st));
+  JZ_CUDA(cudaFreeAsync(superbeg, st));
+  *superbeg_out = nullptr;
+  (void)npts;
 }
 
 }  // namespace jz

@@ -623,3 +623,33 @@ def test_search_host_z_streamed():
         assert np.array_equal(np.sort(rg), np.arange(len(pos)))
         io, do = knn_grid(pos, k, box)
         _assert_same(idx, d2, io[rg], do[rg])
+
+
+@pytest.mark.parametrize("kind,box,r", [("clustered", 1.0, 0.01), ("uniform", None, 0.02), ("clustered", 1.0, 0.3)])
+def test_fof_group_order(kind, box, r):
+    """P:L498 group order: a stable sort of the points by group root -- every group (oracle
+    components) is one contiguous block, blocks in z order of their roots, z order inside."""
+    import paper_2604_05885_b200 as jz
+    from oracle import fof_labels
+
+    pos = (clustered_points if kind == "clustered" else uniform_points)(30_000, 61, 1.0)
+    ix = jz.KnnIndex(torch.from_numpy(pos).cuda(), box=box)
+    lab, _ = ix.fof(r, 2)
+    order, beg = ix.fof_group_order()
+    perm = ix.perm()
+    ix.free()
+    order, beg, lab = order.cpu().numpy(), beg.cpu().numpy(), lab.cpu().numpy()
+    want = fof_labels(pos, r, box)
+    assert np.array_equal(lab, want)
+    assert np.array_equal(np.sort(order), np.arange(len(pos)))
+    zpos = np.empty(len(pos), np.int64)
+    zpos[perm] = np.arange(len(pos))
+    assert beg[0] == 0 and beg[-1] == len(pos) and np.all(np.diff(beg) > 0)
+    assert len(beg) - 1 == len(np.unique(want))
+    heads = []
+    for g in range(len(beg) - 1):
+        blk = order[beg[g]:beg[g + 1]]
+        assert np.all(want[blk] == want[blk[0]])
+        assert np.all(np.diff(zpos[blk]) > 0)
+        heads.append(zpos[blk[0]])
+    assert np.all(np.diff(heads) > 0)
