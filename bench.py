@@ -228,8 +228,7 @@ def run_single(args):
             "config": {"workload": args.config, "n_points": n, "k": k, "box": "periodic L=1" if box else "open",
                        "distribution": c["kind"], "order": "input",
                        "l2": _l2_note(n, k)},
-            "roofline": roofline, "stages_ms": st_ms, "dominant_stage": dominant, "evals_per_query": evals / n, "inserts_per_query": inserts / n,
-            "walk_per_item": {kk: v / max(1, stages[-1]["walk"]["items"]) for kk, v in stages[-1]["walk"].items()},
+            "roofline": roofline, "stages_ms": st_ms, "dominant_stage": dominant, "evals_per_query": evals / n,
             "gpu_launches": int(launches * args.steps), "clocks": clocks}
     if not args.profile and not args.no_e2e:
         line["e2e"] = run_e2e(args, pos, box, k)
