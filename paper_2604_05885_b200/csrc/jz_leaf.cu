@@ -55,6 +55,10 @@ static_assert(JZ_LCAP >= kMaxLeaf, "a leaf must fit the staging buffer");
 #define JZ_STATS 0  // per-lane walk counters (appends, merge rounds, compactions): diagnostic builds (tools/mkvar.py)
 #endif
 
+#ifndef JZ_VEC_ROWS
+#define JZ_VEC_ROWS 2  // 2: rows staged in shared memory, 8 whole rows per warp store; 1: 128-bit stores per lane; 0: scalar (119.5 -> 107.3 -> 106.8 ms)
+#endif
+
 #ifndef JZ_FOF_FULL
 #define JZ_FOF_FULL 0  // 1: link whole (item, leaf) pairs within R_link without evaluating them (measured slower at 10^8 C4: 104 vs 89 ms)
 #endif
@@ -883,21 +887,62 @@ __global__ void __launch_bounds__(kLThreads, MinBlocks<K>::v) k_leaf(LeafPK a, D
       }
     }
   }
-  if (act) {
+  {
     u64 T[K];
 #pragma unroll
-    for (int j = 0; j < K; ++j) T[j] = j < L.nl ? B.lk[j][lane] : ~0ull;
+    for (int j = 0; j < K; ++j) T[j] = (act && j < L.nl) ? B.lk[j][lane] : ~0ull;
     bitonic_sort<K>(T);
-    int32_t *oi = a.out_idx + row * a.ldo + a.col0;
-    float *od = a.out_d2 + row * a.ldo + a.col0;
+    if (JZ_VEC_ROWS == 2 && a.k == K && ((a.ldo | a.col0) & 3) == 0) {
+      // rows through shared memory (the log area is free now): one warp store covers 8 whole
+      // rows (4 lanes x 16 B each) instead of 32 partial rows. Row stride K + 4 words keeps the
+      // 16-byte alignment (4-way bank conflicts on the writes)
+      constexpr int RS = K + 4;
+      static_assert(2 * 32 * RS * 4 <= LogCap<K>::C * 32 * 8, "row staging must fit the log area");
+      unsigned *sidx = reinterpret_cast<unsigned *>(&B.lk[0][0]);  // [32][RS] idx, then [32][RS] d2
+      unsigned *sd2 = sidx + 32 * RS;
+      __syncwarp();
 #pragma unroll
-    for (int j = 0; j < K; ++j) {
-      if (j < a.k) {
-        oi[j] = (int32_t)((unsigned)(T[j] & 0xffffffffu) - 1u);
-        od[j] = __uint_as_float((unsigned)(T[j] >> 32));
+      for (int j = 0; j < K; ++j) {
+        sidx[lane * RS + j] = (unsigned)(T[j] & 0xffffffffu) - 1u;
+        sd2[lane * RS + j] = (unsigned)(T[j] >> 32);
+      }
+      __syncwarp();
+      constexpr int LPR = K / 4;  // lanes per row (16 B each)
+#pragma unroll
+      for (int r0 = 0; r0 < 32; r0 += 32 / LPR) {
+        const int r = r0 + lane / LPR, c = lane % LPR;
+        const int64_t rr = __shfl_sync(0xffffffffu, row, r);
+        const int ra = __shfl_sync(0xffffffffu, (int)act, r);
+        if (ra) {
+          reinterpret_cast<uint4 *>(a.out_idx + rr * a.ldo + a.col0)[c] = reinterpret_cast<const uint4 *>(sidx + r * RS)[c];
+          reinterpret_cast<uint4 *>(a.out_d2 + rr * a.ldo + a.col0)[c] = reinterpret_cast<const uint4 *>(sd2 + r * RS)[c];
+        }
+      }
+    } else if (act) {
+      int32_t *oi = a.out_idx + row * a.ldo + a.col0;
+      float *od = a.out_d2 + row * a.ldo + a.col0;
+      if (JZ_VEC_ROWS && a.k == K && ((a.ldo | a.col0) & 3) == 0) {
+        // full 16-byte aligned rows: 128-bit stores (K / 4 per array instead of K scalar stores)
+#pragma unroll
+        for (int j = 0; j < K; j += 4) {
+          reinterpret_cast<int4 *>(oi)[j / 4] = make_int4(
+              (int32_t)((unsigned)(T[j] & 0xffffffffu) - 1u), (int32_t)((unsigned)(T[j + 1] & 0xffffffffu) - 1u),
+              (int32_t)((unsigned)(T[j + 2] & 0xffffffffu) - 1u), (int32_t)((unsigned)(T[j + 3] & 0xffffffffu) - 1u));
+          reinterpret_cast<float4 *>(od)[j / 4] =
+              make_float4(__uint_as_float((unsigned)(T[j] >> 32)), __uint_as_float((unsigned)(T[j + 1] >> 32)),
+                          __uint_as_float((unsigned)(T[j + 2] >> 32)), __uint_as_float((unsigned)(T[j + 3] >> 32)));
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+          if (j < a.k) {
+            oi[j] = (int32_t)((unsigned)(T[j] & 0xffffffffu) - 1u);
+            od[j] = __uint_as_float((unsigned)(T[j] >> 32));
+          }
+        }
       }
     }
-    if (a.out_row_gidx) a.out_row_gidx[row] = __float_as_int(qw);
+    if (act && a.out_row_gidx) a.out_row_gidx[row] = __float_as_int(qw);
   }
 }
 

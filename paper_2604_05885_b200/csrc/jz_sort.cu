@@ -260,8 +260,14 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_onesweep(
 // even at halo centres) are then in input order; a fix-up orders each such run by (key, index),
 // which makes the result the stable argsort of the full keys. Runs longer than
 // kSegBlock (massive duplicates) fall back to the 8-pass sort of the full keys.
+#ifndef JZ_S32_IPT
+#define JZ_S32_IPT 16
+#endif
+#ifndef JZ_S32_MINB
+#define JZ_S32_MINB 3
+#endif
 constexpr int kS32Threads = 256;
-constexpr int kS32IPT = 16;
+constexpr int kS32IPT = JZ_S32_IPT;
 constexpr int kS32Tile = kS32Threads * kS32IPT;
 constexpr int kS32Passes = 5;     // pass 0: key bits 23..30; passes 1-4: the bytes of hi = key >> 31
 constexpr int kLoShift = 23;
@@ -307,7 +313,7 @@ __device__ __forceinline__ float4 load_point(const float *__restrict__ pos, int 
 // One-sweep pass over (hi, index) pairs. Non-first passes bring the tile into shared memory with
 // 16-byte asynchronous copies (every load of the tile in flight at once), then rank as above.
 template <bool FIRST, bool LAST>
-__global__ void __launch_bounds__(kS32Threads, 3) k_onesweep32(
+__global__ void __launch_bounds__(kS32Threads, JZ_S32_MINB) k_onesweep32(
     const float *__restrict__ pos, int stride, int gidx_mode, int64_t gidx_base, Frame f,
     const uint32_t *__restrict__ kin, const uint32_t *__restrict__ vin, uint32_t *__restrict__ kout,
     uint32_t *__restrict__ vout, uint64_t *__restrict__ keys_out, float4 *__restrict__ pts_out, int64_t n, int shift,
