@@ -169,7 +169,7 @@ def run_single(args):
     d2 = torch.empty((n, k), dtype=torch.float32, device=dev)
     jz.set_timing(True)
 
-    prm = {"nmax0": args.nmax0} if args.nmax0 else None
+    prm = {k_: v_ for k_, v_ in (("nmax0", args.nmax0), ("coarsen", args.coarsen), ("ntarget", args.ntarget)) if v_} or None
 
     def step():
         ix = jz.KnnIndex(d_pos, box=box, params=prm)
@@ -383,6 +383,8 @@ def main():
     ap.add_argument("--config", default="C4")
     ap.add_argument("--n", type=int, default=None, help="override the point count (tests)")
     ap.add_argument("--nmax0", type=int, default=0, help="leaf capacity N_max^(0) override (tuning experiments)")
+    ap.add_argument("--coarsen", type=int, default=0, help="plane coarsening c override (tuning experiments)")
+    ap.add_argument("--ntarget", type=int, default=0, help="N_target override (tuning experiments)")
     ap.add_argument("--ref-rows", type=int, default=1_000_000)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
