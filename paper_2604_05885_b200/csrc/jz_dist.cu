@@ -549,7 +549,7 @@ namespace jz {
 // sample-splitter Morton-range partition of L112-114, on a jz_comm (NCCL or logical ranks).
 constexpr int kSampTotal = 16384;  // all ranks' key samples are sorted by one CTA
 #ifndef JZ_QBOX_NODES
-#define JZ_QBOX_NODES 16384
+#define JZ_QBOX_NODES 65536
 #endif
 #ifndef JZ_REG_GHOST
 #define JZ_REG_GHOST 50
@@ -642,6 +642,52 @@ __global__ void k_merge_rows(const int32_t *__restrict__ idx2, const float *__re
     if (c == 0 && rowg2[r] != __float_as_int(pts[i].w)) *bad = 1;
     idx[i * k + c] = idx2[t];
     d2[i * k + c] = d22[t];
+  }
+}
+
+// query-only points of a joint tree (the library's convention: negative id)
+__global__ void k_query_only(float4 *__restrict__ p, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i].w = __int_as_float(-1);
+}
+
+// row t of the ghost walk (query bpos[t], reported by its input row t of the joint tree) merged with
+// the query's local row: the k smallest of the two (d2, id)-sorted rows (d2 >= 0: bit order ==
+// float order; ids are distinct between local and ghost points)
+__global__ void k_merge_ghost_rows(const int32_t *__restrict__ gi, const float *__restrict__ gd,
+                                   const int32_t *__restrict__ growg, int kg, const int32_t *__restrict__ bpos,
+                                   int64_t nb, int k, int32_t *__restrict__ idx, float *__restrict__ d2,
+                                   int32_t *__restrict__ ti, float *__restrict__ td, int *__restrict__ bad) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nb; t += (int64_t)gridDim.x * blockDim.x) {
+    if (growg[t] != (int32_t)t) *bad = 1;
+    const int64_t i = bpos[t];
+    const int32_t *li = idx + i * k;
+    const float *ld = d2 + i * k;
+    const int32_t *hi = gi + t * kg;
+    const float *hd = gd + t * kg;
+    int a = 0, b = 0;
+    for (int c = 0; c < k; ++c) {
+      bool take_local;
+      if (b >= kg) take_local = true;
+      else if (a >= k) take_local = false;
+      else {
+        const unsigned x = __float_as_uint(ld[a]), y = __float_as_uint(hd[b]);
+        take_local = x < y || (x == y && li[a] < hi[b]);
+      }
+      if (take_local) {
+        ti[t * k + c] = li[a];
+        td[t * k + c] = ld[a];
+        ++a;
+      } else {
+        ti[t * k + c] = hi[b];
+        td[t * k + c] = hd[b];
+        ++b;
+      }
+    }
+    for (int c = 0; c < k; ++c) {
+      idx[i * k + c] = ti[t * k + c];
+      d2[i * k + c] = td[t * k + c];
+    }
   }
 }
 
@@ -1013,45 +1059,83 @@ int jz_knn_query_dist(jz_knn_index *ix, int k, int order, int32_t *out_idx, floa
         exclusive_scan_i32_to_i64(flag, off, m, st);
         nreq = read_i64(off + m, st);
         if (nreq > 0) {
-          // 10. second walk over local + ghost points with the flagged points as the only queries
-          //     (their local rows are replaced: exact over every point within their radius)
-          float4 *all = S.get<float4>(m + nghost);
           int32_t *bpos = S.get<int32_t>(nreq);
-          k_gather_flagged<<<grid_for(m, 256), 256, 0, st>>>(ix->pts, flag, off, m, 1, all, bpos);
-          JZ_LAUNCH_CHECK();
-          k_gather_flagged<<<grid_for(m, 256), 256, 0, st>>>(ix->pts, flag, off, m, 0, all + nreq, nullptr);
-          JZ_LAUNCH_CHECK();
-          JZ_CUDA(cudaMemcpyAsync(all + m, ghosts, nghost * sizeof(float4), cudaMemcpyDeviceToDevice, st));
           jz_knn_index *ix2 = nullptr;
           try {
-            mark("flags+gather");
-            // ghosts are a thin shell outside this rank's Morton range: sparse in key space, they would
-            // form a few huge nodes (long NodeToNode lists); the regularisation of P:L255-270 (F3)
-            // splits nodes far larger than the typical node
-            jz_knn_params p2 = ix->prm_frame;
-            if (p2.reg_fmax <= 0) p2.reg_fmax = kRegGhost;
-            ix2 = build_impl(reinterpret_cast<const float *>(all), m + nghost, 4, 1, nreq, boxp, &p2, st);
-            mark("second build");
-            int32_t *idx2 = S.get<int32_t>(nreq * k);
-            float *d22 = S.get<float>(nreq * k);
-            int32_t *rowg2 = S.get<int32_t>(nreq);
-            ck(jz_knn_query(ix2, k, JZ_ORDER_Z, idx2, d22, rowg2, s));
-            mark("re-walk");
-            if (prof) {
-              float tm[6];
-              int64_t ev = 0;
-              jz_knn_stage_times(ix2, tm, &ev);
-              fprintf(stderr, "rank %d re-walk: planes %d n2n %.2f ms leaf %.2f ms evals/query %.0f\n", r,
-                      (int)ix2->planes.size(), tm[3], tm[4], (double)ev / (double)nreq);
+            // JZ_REWALK_GHOST=1: walk the flagged queries against the ghosts only and merge with the
+            // local rows (no second tree over local + ghosts); measured slower and erratic at 10^8
+            // (ghost walk ~10 ms: the flagged queries are sparse in z order, so their 32-query items
+            // span large boxes), kept as an option
+            static const bool ghost_only = getenv("JZ_REWALK_GHOST") != nullptr;
+            if (local_rows && ghost_only) {
+              // 10. the flagged queries walked against the ghost points only (a joint tree of
+              //     nreq query-only points + the ghosts), then each row is merged with the query's
+              //     exact local row: the union's k smallest (d2, id) pairs are the global row,
+              //     since every point within the local k-th distance is local or a ghost
+              float4 *all = S.get<float4>(nreq + nghost);
+              k_gather_flagged<<<grid_for(m, 256), 256, 0, st>>>(ix->pts, flag, off, m, 1, all, bpos);
+              JZ_LAUNCH_CHECK();
+              k_query_only<<<grid_for(nreq, 256), 256, 0, st>>>(all, nreq);
+              JZ_LAUNCH_CHECK();
+              JZ_CUDA(cudaMemcpyAsync(all + nreq, ghosts, nghost * sizeof(float4), cudaMemcpyDeviceToDevice, st));
+              mark("flags+gather");
+              // ghosts are thin shells outside this rank's Morton range, sparse in key space: the
+              // regularisation of P:L255-270 (F3) splits the huge nodes they would form
+              jz_knn_params p2 = ix->prm_frame;
+              if (p2.reg_fmax <= 0) p2.reg_fmax = kRegGhost;
+              ix2 = build_impl(reinterpret_cast<const float *>(all), nreq + nghost, 4, 1, nreq, boxp, &p2, st);
+              mark("ghost build");
+              const int kg = (int)(k < nghost ? k : nghost);
+              int32_t *idx2 = S.get<int32_t>(nreq * kg);
+              float *d22 = S.get<float>(nreq * kg);
+              int32_t *rowg2 = S.get<int32_t>(nreq);
+              ck(jz_knn_query(ix2, kg, JZ_ORDER_Z, idx2, d22, rowg2, s));
+              mark("ghost walk");
+              if (prof) {
+                float tm[6];
+                int64_t ev = 0;
+                jz_knn_stage_times(ix2, tm, &ev);
+                fprintf(stderr, "rank %d ghost walk: planes %d n2n %.2f ms leaf %.2f ms evals/query %.0f\n", r,
+                        (int)ix2->planes.size(), tm[3], tm[4], (double)ev / (double)nreq);
+              }
+              int *bad = S.get<int>(1);
+              JZ_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), st));
+              int32_t *tmpi = S.get<int32_t>(nreq * k);
+              float *tmpd = S.get<float>(nreq * k);
+              k_merge_ghost_rows<<<grid_for(nreq, 128), 128, 0, st>>>(idx2, d22, rowg2, kg, bpos, nreq, k, idx1, d21,
+                                                                       tmpi, tmpd, bad);
+              JZ_LAUNCH_CHECK();
+              int hb = 0;
+              JZ_CUDA(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+              JZ_CUDA(cudaStreamSynchronize(st));
+              if (hb) throw Error(JZ_ECUDA, "internal: ghost rows out of order");
+            } else {
+              // 10. the flagged queries walked over local + ghost points (a second tree with those
+              //     queries first); their rows replace the local rows (a rank with < k local
+              //     points: every local query is flagged)
+              float4 *all = S.get<float4>(m + nghost);
+              k_gather_flagged<<<grid_for(m, 256), 256, 0, st>>>(ix->pts, flag, off, m, 1, all, bpos);
+              JZ_LAUNCH_CHECK();
+              k_gather_flagged<<<grid_for(m, 256), 256, 0, st>>>(ix->pts, flag, off, m, 0, all + nreq, nullptr);
+              JZ_LAUNCH_CHECK();
+              JZ_CUDA(cudaMemcpyAsync(all + m, ghosts, nghost * sizeof(float4), cudaMemcpyDeviceToDevice, st));
+              jz_knn_params p2 = ix->prm_frame;
+              if (p2.reg_fmax <= 0) p2.reg_fmax = kRegGhost;
+              ix2 = build_impl(reinterpret_cast<const float *>(all), m + nghost, 4, 1, nreq, boxp, &p2, st);
+              int32_t *idx2 = S.get<int32_t>(nreq * k);
+              float *d22 = S.get<float>(nreq * k);
+              int32_t *rowg2 = S.get<int32_t>(nreq);
+              ck(jz_knn_query(ix2, k, JZ_ORDER_Z, idx2, d22, rowg2, s));
+              int *bad = S.get<int>(1);
+              JZ_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), st));
+              k_merge_rows<<<grid_for(nreq * k, 256), 256, 0, st>>>(idx2, d22, rowg2, bpos, nreq, k, ix->pts, idx1, d21,
+                                                                    bad);
+              JZ_LAUNCH_CHECK();
+              int hb = 0;
+              JZ_CUDA(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+              JZ_CUDA(cudaStreamSynchronize(st));
+              if (hb) throw Error(JZ_ECUDA, "internal: re-walked rows out of order");
             }
-            int *bad = S.get<int>(1);
-            JZ_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), st));
-            k_merge_rows<<<grid_for(nreq * k, 256), 256, 0, st>>>(idx2, d22, rowg2, bpos, nreq, k, ix->pts, idx1, d21, bad);
-            JZ_LAUNCH_CHECK();
-            int hb = 0;
-            JZ_CUDA(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
-            JZ_CUDA(cudaStreamSynchronize(st));
-            if (hb) throw Error(JZ_ECUDA, "internal: re-walked rows out of order");
           } catch (...) {
             jz_knn_free(ix2);
             cudaFreeAsync(ghosts, st);
