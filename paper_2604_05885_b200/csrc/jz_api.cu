@@ -357,19 +357,29 @@ jz_knn_index *jz::build_impl(const float *pos, int64_t n, int stride, int gidx_m
       fprintf(stderr, "build n=%lld %-8s %8.2f ms\n", (long long)n, w, t - tb);
       tb = t;
     };
+    jz::NvtxRange nv_build("jz build");
     rec(ix, 0);
     jz::Frame frame;
-    jz::compute_frame(pos, n, stride, ix->D, prm, &frame, st);
+    {
+      jz::NvtxRange nv("jz A1 frame");
+      jz::compute_frame(pos, n, stride, ix->D, prm, &frame, st);
+    }
     bmark("frame");
     rec(ix, 1);
     JZ_CUDA(cudaMallocAsync(&ix->pts, n * sizeof(float4), st));
     JZ_CUDA(cudaMallocAsync(&ix->keys, n * sizeof(uint64_t), st));
     JZ_CUDA(cudaMallocAsync(&ix->perm, n * sizeof(int32_t), st));
     bmark("alloc");
-    jz::sort_points(pos, n, stride, gidx_mode, 0, frame, ix->keys, ix->perm, ix->pts, st);
+    {
+      jz::NvtxRange nv("jz A2-A3 sort");
+      jz::sort_points(pos, n, stride, gidx_mode, 0, frame, ix->keys, ix->perm, ix->pts, st);
+    }
     bmark("sort");
     rec(ix, 2);
-    jz::build_planes(ix->keys, ix->pts, n, prm, ix->planes, st);
+    {
+      jz::NvtxRange nv("jz A4-A8 planes");
+      jz::build_planes(ix->keys, ix->pts, n, prm, ix->planes, st);
+    }
     bmark("planes");
     split_types(ix, gidx_mode != 0);
     bmark("types");
@@ -472,13 +482,17 @@ static int query_impl(jz_knn_index *ix, int k, int order, int32_t *out_idx, floa
   cudaStream_t st = (cudaStream_t)s;
   ix->st = st;
   if (ix->n_query == 0) return JZ_OK;
+  jz::NvtxRange nv_query("jz query");
   rec(ix, 4);
   jz::IList il;
   float *rmax2 = nullptr;
   int32_t *superbeg = nullptr;
   // walk down to plane 1: its nodes are the receiving parents of LeafToLeaf (jz_leaf.cu)
-  jz::walk_to(ix->planes, ix->D, k, ix->prm.ngr, ix->prm.flags, 1, il, &rmax2, &superbeg, st, -1.f,
-              ix->n_query < ix->n ? ix->qbeg : nullptr);
+  {
+    jz::NvtxRange nv("jz A9-A10 NodeToNode");
+    jz::walk_to(ix->planes, ix->D, k, ix->prm.ngr, ix->prm.flags, 1, il, &rmax2, &superbeg, st, -1.f,
+                ix->n_query < ix->n ? ix->qbeg : nullptr);
+  }
   rec(ix, 5);
   if (!ix->d_evals) JZ_CUDA(cudaMallocAsync(&ix->d_evals, 16 * sizeof(unsigned long long), st));
   JZ_CUDA(cudaMemsetAsync(ix->d_evals, 0, 16 * sizeof(unsigned long long), st));
@@ -506,7 +520,10 @@ static int query_impl(jz_knn_index *ix, int k, int order, int32_t *out_idx, floa
   la.chunks = chunks;
   la.nq = ix->n_query;
   la.on_rows = on_rows;
-  jz::leaf_to_leaf(la, ix->D, st);
+  {
+    jz::NvtxRange nv("jz A11-A12 LeafToLeaf");
+    jz::leaf_to_leaf(la, ix->D, st);
+  }
   rec(ix, 6);
   il.release(st);
   if (rmax2) JZ_CUDA(cudaFreeAsync(rmax2, st));
@@ -705,6 +722,7 @@ int jz_fof(jz_knn_index *ix, float r_link, int32_t min_count, int32_t *labels, i
   JZ_CUDA(cudaMallocAsync(&minlab, n * sizeof(int32_t), st));
   k_fof_init<<<jz::grid_for(n, 256), 256, 0, st>>>(par, minlab, n);
   JZ_LAUNCH_CHECK();
+  jz::NvtxRange nv_fof("jz friends-of-friends");
   // node-level walk: ParentToNode, three-case NodeToNode with node links; linked
   // leaves' points start in their group (par), the remaining pairs go to the leaf stage
   jz::fof_walk(ix->planes, ix->D, ix->prm.ngr, b2, il, &superbeg, par, n, st);

@@ -14,6 +14,7 @@
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <stdexcept>
 #include <string>
 
@@ -37,6 +38,15 @@ struct Error : std::runtime_error {
                         std::string(#call) + ": " + cudaGetErrorString(e_) + " at " + __FILE__ + ":" +      \
                             std::to_string(__LINE__));                                                     \
   } while (0)
+
+// NVTX range for the host-side phases (visible in Nsight Systems / ncu --nvtx; no cost without
+// an attached tool)
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange &) = delete;
+  NvtxRange &operator=(const NvtxRange &) = delete;
+};
 
 // every kernel launch is followed by JZ_LAUNCH_CHECK(); it also counts launches (jz_launch_count)
 void count_launch();

@@ -804,6 +804,7 @@ int jz_knn_build_dist(jz_comm *comm, const float *pos, int64_t n, int64_t gidx_b
     ~Guard() { c->leave(st); }
   } guard{(comm->enter(), comm), st};
   try {
+    NvtxRange nv("jz build_dist");
     const int R = comm->size, r = comm->rank;
     double t0 = now_ms();
     Dom D{};
@@ -935,6 +936,7 @@ int jz_knn_query_dist(jz_knn_index *ix, int k, int order, int32_t *out_idx, floa
     ~Guard() { c->leave(st); }
   } guard{(ix->comm->enter(), ix->comm), st};
   try {
+    NvtxRange nv("jz query_dist");
     Comm *comm = ix->comm;
     const int R = comm->size, r = comm->rank;
     const int64_t m = ix->empty ? 0 : ix->n;
