@@ -14,6 +14,7 @@
 //   k_segsort     sort each receiver's segment by (rlow, isrc) (P:L396 bitonic network).
 // All bounds are squared FP32 values that bound the canonical d2 exactly (jz_common.cuh).
 #include <climits>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -210,6 +211,81 @@ __global__ void __launch_bounds__(kN2NWarps * 32) k_n2n(const int32_t *__restric
   }
 }
 
+// ---- flat variant: one thread per receiving child (all lanes busy whatever the fan-out c); the
+// source boxes come through L1 (consecutive children share their parent's list, so a warp mostly
+// reads the same boxes). Same decisions as k_n2n, per child instead of per 32-child chunk.
+#ifndef JZ_N2N_FLAT
+#define JZ_N2N_FLAT 1
+#endif
+__global__ void k_child_parent(const int32_t *__restrict__ pbeg, int64_t npar, int32_t *__restrict__ cpar) {
+  for (int64_t P = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; P < npar; P += (int64_t)gridDim.x * blockDim.x)
+    for (int c = pbeg[P]; c < pbeg[P + 1]; ++c) cpar[c] = (int32_t)P;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) k_n2n_flat(const int32_t *__restrict__ cpar, int64_t nchild,
+                                                  const int32_t *__restrict__ pbeg, const int64_t *__restrict__ ispl,
+                                                  const int32_t *__restrict__ isrc, const float *__restrict__ rlow,
+                                                  const NodeBox *__restrict__ cbox, Dom D, int k, int sorted, int early,
+                                                  float *__restrict__ rmax2, int32_t *__restrict__ cnt,
+                                                  const int64_t *__restrict__ ispl_out, int32_t *__restrict__ isrc_out,
+                                                  float *__restrict__ rlow_out, const uint8_t *__restrict__ qf) {
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nchild; c += (int64_t)gridDim.x * blockDim.x) {
+    if (qf && !qf[c]) {  // no queries below: no list
+      if (MODE == RMAX) rmax2[c] = 0.f;
+      if (MODE == COUNT) cnt[c] = 0;
+      continue;
+    }
+    const int J = cpar[c];
+    const NodeBox mb = cbox[c];
+    CountHeap h;
+    float R = INFINITY;
+    if (MODE == RMAX) {
+#pragma unroll
+      for (int j = 0; j < kHeap; ++j) {
+        h.r[j] = INFINITY;
+        h.c[j] = 0;
+      }
+      h.tot = 0;
+    } else {
+      R = rmax2[c];
+    }
+    int count = 0;
+    int64_t wp = MODE == INSERT ? ispl_out[c] : 0;
+    const int64_t eb = ispl[J], ee = ispl[J + 1];
+    for (int64_t e = eb; e < ee; ++e) {
+      const float rl = rlow[e];
+      if (early && (MODE == RMAX ? !(rl < R) : !(rl <= R))) {
+        if (sorted) break;
+        continue;
+      }
+      const int S = isrc[e];
+      for (int s = pbeg[S]; s < pbeg[S + 1]; ++s) {
+        const NodeBox sbx = cbox[s];
+        if (MODE == RMAX) {
+          const float r2 = box_dup2(mb, sbx, D);
+          if (r2 < R) {
+            heap_insert(h, r2, box_count(sbx), k);
+            R = heap_radius(h, k);
+          }
+        } else {
+          const float dl = box_dlow2(mb, sbx, D);
+          if (dl <= R) {
+            if (MODE == COUNT) ++count;
+            else {
+              isrc_out[wp] = s;
+              rlow_out[wp] = dl;
+              ++wp;
+            }
+          }
+        }
+      }
+    }
+    if (MODE == RMAX) rmax2[c] = R;
+    if (MODE == COUNT) cnt[c] = count;
+  }
+}
+
 // receivers holding queries: leaves from the query leaf starts, upper planes by OR over children
 __global__ void k_qflag_leaf(const int32_t *__restrict__ qbeg, int64_t n, uint8_t *__restrict__ f) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -316,16 +392,31 @@ void walk_to(const std::vector<Plane> &planes, const Dom &D, int k, int ngr, uns
     JZ_CUDA(cudaMallocAsync(&cnt, pl.nnodes * sizeof(int32_t), st));
     const int srt = do_sort ? 1 : 0;
     const int ee = early ? 1 : 0;
+    int32_t *cpar = nullptr;
+    const bool flat = JZ_N2N_FLAT && !getenv("JZ_N2N_WARP");
+    if (flat) {
+      JZ_CUDA(cudaMallocAsync(&cpar, (pl.nnodes > 0 ? pl.nnodes : 1) * sizeof(int32_t), st));
+      k_child_parent<<<grid_for(npar, 256), 256, 0, st>>>(pbeg, npar, cpar);
+      JZ_LAUNCH_CHECK();
+    }
+    const unsigned fb = (unsigned)grid_for(pl.nnodes, 256);
     if (fixed_r2 >= 0.f) {  // fixed-radius walk (friends-of-friends): every node keeps r^2
       k_fill_f32<<<grid_for(pl.nnodes, 256), 256, 0, st>>>(rmax2, pl.nnodes, fixed_r2);
+    } else if (flat) {
+      k_n2n_flat<RMAX><<<fb, 256, 0, st>>>(cpar, pl.nnodes, pbeg, il.ispl, il.isrc, il.rlow, pl.box, D, k, srt, ee, rmax2,
+                                             nullptr, nullptr, nullptr, nullptr, qf[p]);
     } else {
       k_n2n<RMAX><<<(unsigned)ceil_div(npar, kN2NWarps), kN2NWarps * 32, 0, st>>>(pbeg, npar, il.ispl, il.isrc, il.rlow,
                                                                                 pl.box, D, k, srt, ee, rmax2, nullptr,
                                                                                 nullptr, nullptr, nullptr, qf[p]);
     }
     JZ_LAUNCH_CHECK();
-    k_n2n<COUNT><<<(unsigned)ceil_div(npar, kN2NWarps), kN2NWarps * 32, 0, st>>>(pbeg, npar, il.ispl, il.isrc, il.rlow, pl.box, D, k, srt, ee,
-                                                         rmax2, cnt, nullptr, nullptr, nullptr, qf[p]);
+    if (flat)
+      k_n2n_flat<COUNT><<<fb, 256, 0, st>>>(cpar, pl.nnodes, pbeg, il.ispl, il.isrc, il.rlow, pl.box, D, k, srt, ee,
+                                              rmax2, cnt, nullptr, nullptr, nullptr, qf[p]);
+    else
+      k_n2n<COUNT><<<(unsigned)ceil_div(npar, kN2NWarps), kN2NWarps * 32, 0, st>>>(pbeg, npar, il.ispl, il.isrc, il.rlow, pl.box, D, k, srt, ee,
+                                                           rmax2, cnt, nullptr, nullptr, nullptr, qf[p]);
     JZ_LAUNCH_CHECK();
     IList nl;
     nl.nrecv = pl.nnodes;
@@ -334,9 +425,14 @@ void walk_to(const std::vector<Plane> &planes, const Dom &D, int k, int ngr, uns
     nl.total = read_i64(nl.ispl + pl.nnodes, st);
     JZ_CUDA(cudaMallocAsync(&nl.isrc, (nl.total > 0 ? nl.total : 1) * sizeof(int32_t), st));
     JZ_CUDA(cudaMallocAsync(&nl.rlow, (nl.total > 0 ? nl.total : 1) * sizeof(float), st));
-    k_n2n<INSERT><<<(unsigned)ceil_div(npar, kN2NWarps), kN2NWarps * 32, 0, st>>>(pbeg, npar, il.ispl, il.isrc, il.rlow, pl.box, D, k, srt, ee,
-                                                          rmax2, nullptr, nl.ispl, nl.isrc, nl.rlow, qf[p]);
+    if (flat)
+      k_n2n_flat<INSERT><<<fb, 256, 0, st>>>(cpar, pl.nnodes, pbeg, il.ispl, il.isrc, il.rlow, pl.box, D, k, srt, ee,
+                                               rmax2, nullptr, nl.ispl, nl.isrc, nl.rlow, qf[p]);
+    else
+      k_n2n<INSERT><<<(unsigned)ceil_div(npar, kN2NWarps), kN2NWarps * 32, 0, st>>>(pbeg, npar, il.ispl, il.isrc, il.rlow, pl.box, D, k, srt, ee,
+                                                            rmax2, nullptr, nl.ispl, nl.isrc, nl.rlow, qf[p]);
     JZ_LAUNCH_CHECK();
+    if (cpar) JZ_CUDA(cudaFreeAsync(cpar, st));
     if (do_sort) {
       k_segsort<<<grid_for(pl.nnodes, kSegWarps, 148 * 16), kSegWarps * 32, 0, st>>>(nl.ispl, nl.nrecv, nl.isrc,
                                                                                      nl.rlow);
