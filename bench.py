@@ -230,6 +230,9 @@ def run_single(args):
                        "l2": _l2_note(n, k)},
             "roofline": roofline, "stages_ms": st_ms, "dominant_stage": dominant, "evals_per_query": evals / n,
             "gpu_launches": int(launches * args.steps), "clocks": clocks}
+    w = stages[-1].get("walk", {})
+    if w.get("items"):  # per 32-query work item (appends / merge rounds / compactions need a JZ_STATS build)
+        line["walk_per_item"] = {kk: w[kk] / w["items"] for kk in w if kk != "items"}
     if not args.profile and not args.no_e2e:
         line["e2e"] = run_e2e(args, pos, box, k)
     if not args.profile and not args.no_cpu_baseline:

@@ -742,6 +742,116 @@ __device__ __forceinline__ void own_pass(const LeafPK &a, const Dom &D, WarpBuf<
   }
 }
 
+// ---------------------------------------------------------------- exact own pass (JZ_OWN_EXACT)
+// The own block (the sources of the leaves holding the warp's queries, "the leaf's own
+// points") is where most candidates fall below a loose k-th value: with the log it cost ~80% of
+// the appends and ~45% of the merge rounds of an item. Here it is done in two fixed-cost sweeps:
+//  A. every lane merges the d2 of 8 sources at a time into its sorted list F by a network (sort
+//     the 8 values, min against F's reversed tail, bitonic merge): no log, no divergence; after
+//     the sweep F holds the K smallest values of the own block exactly;
+//  B. the block is evaluated again and every candidate with d2 <= F[K-1] is logged: the K
+//     smallest keys (+ exact ties) with no merges (F is already final for the block).
+// The walk then starts from the exact own-block k-th value and a log of ~K entries.
+#ifndef JZ_OWN_EXACT
+#define JZ_OWN_EXACT 1
+#endif
+
+// F (ascending, K values) := the K smallest of F and N (8 values, no NaN)
+template <int K>
+__device__ __forceinline__ void net_merge8(float (&F)[K], float (&N)[8]) {
+  bitonic_sort_f<8>(N);
+  if (!__any_sync(0xffffffffu, N[0] < F[K - 1])) return;
+  constexpr int T = K < 8 ? K : 8;
+#pragma unroll
+  for (int i = 0; i < T; ++i) F[K - 1 - i] = fminf(F[K - 1 - i], N[i]);  // ascending F, descending N: bitonic
+#pragma unroll
+  for (int s = K / 2; s > 0; s >>= 1) {
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      if ((i & s) == 0) {
+        const float lo = fminf(F[i], F[i + s]), hi = fmaxf(F[i], F[i + s]);
+        F[i] = lo;
+        F[i + s] = hi;
+      }
+    }
+  }
+}
+
+// d2 of the 8 staged sources [j, j + 8): packed (no wrap inside the block) or per pair (gen)
+template <int K, bool PER>
+__device__ __forceinline__ void d2x8(const WarpBuf<K> &B, int j, float qx, float qy, float qz, u64 QX, u64 QY, u64 QZ,
+                                     bool gen, const Dom &D, float (&N)[8]) {
+  if (PER && gen) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) N[u] = canon_d2_per(qx, qy, qz, B.x[j + u], B.y[j + u], B.z[j + u], D);
+  } else {
+    d2x4(B.x, B.y, B.z, j, QX, QY, QZ, false, 0ull, 0ull, 0ull, N[0], N[1], N[2], N[3]);
+    d2x4(B.x, B.y, B.z, j + 4, QX, QY, QZ, false, 0ull, 0ull, 0ull, N[4], N[5], N[6], N[7]);
+  }
+}
+
+template <int K, bool LB, bool PER>
+__device__ __forceinline__ void own_exact(const LeafPK &a, const Dom &D, WarpBuf<K> &B, int s0, int s1, int cls_all,
+                                          float qx, float qy, float qz, bool act, Lane<K, LB> &L,
+                                          unsigned long long &nev) {
+  constexpr int C = LogCap<K>::C;
+  const bool gen = PER && cls_all != 0;
+  const u64 QX = pk(qx, qx), QY = pk(qy, qy), QZ = pk(qz, qz);
+  const int nb = (s1 - s0 + kLCap - 1) / kLCap;  // batches
+  // A: exact K smallest values of the block (batches in order; the last one stays staged)
+  for (int b = 0; b < nb; ++b) {
+    const int b0 = s0 + b * kLCap, m = min(kLCap, s1 - b0), mp = (m + 3) & ~3;
+    stage_async<K>(B, 0, a.spts + b0, m, mp);
+    nev += act ? (unsigned)m : 0u;
+    const int np = pad8<K>(B, mp);
+    cpa_wait();
+    __syncwarp();
+#pragma unroll 1
+    for (int j = 0; j < np; j += 8) {
+      float N[8];
+      d2x8<K, PER>(B, j, qx, qy, qz, QX, QY, QZ, gen, D, N);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) N[u] = fminf(N[u], INFINITY);  // NaN padding -> +inf
+      net_merge8<K>(L.F, N);
+    }
+    __syncwarp();
+  }
+  L.kth = act ? L.F[K - 1] : -1.f;
+  // B: log the candidates <= the block's k-th value (last batch first: it is still staged)
+  for (int b = nb - 1; b >= 0; --b) {
+    const int b0 = s0 + b * kLCap, m = min(kLCap, s1 - b0), mp = (m + 3) & ~3;
+    if (b != nb - 1) {
+      stage_async<K>(B, 0, a.spts + b0, m, mp);
+      pad8<K>(B, mp);
+      cpa_wait();
+      __syncwarp();
+    }
+    const int np = (mp + 7) & ~7;
+#pragma unroll 1
+    for (int j = 0; j < np; j += 8) {
+      float N[8];
+      d2x8<K, PER>(B, j, qx, qy, qz, QX, QY, QZ, gen, D, N);
+      const float mn = fminf(fminf(fminf(N[0], N[1]), fminf(N[2], N[3])), fminf(fminf(N[4], N[5]), fminf(N[6], N[7])));
+      if (__any_sync(0xffffffffu, mn <= L.kth)) {
+        const int4 G = *reinterpret_cast<const int4 *>(&B.g[j]);
+        const int4 H = *reinterpret_cast<const int4 *>(&B.g[j + 4]);
+        append<K, LB>(B, L, N[0], G.x);
+        append<K, LB>(B, L, N[1], G.y);
+        append<K, LB>(B, L, N[2], G.z);
+        append<K, LB>(B, L, N[3], G.w);
+        append<K, LB>(B, L, N[4], H.x);
+        append<K, LB>(B, L, N[5], H.y);
+        append<K, LB>(B, L, N[6], H.z);
+        append<K, LB>(B, L, N[7], H.w);
+        // massive exact ties only: the K smallest keys of the log are the block's K smallest keys
+        if (__any_sync(0xffffffffu, L.nl > C - 8)) L.nl = drop_largest<K>(B, L.nl, K);
+      }
+    }
+    __syncwarp();
+  }
+  L.nf = L.nl;
+}
+
 #ifdef JZ_SEED_EXP
 // experiment only (tools/mkvar.py -DJZ_SEED_EXP): per-row k-th d2 seed (ideal-threshold bound)
 __device__ const float *g_seed = nullptr;
@@ -818,7 +928,7 @@ __global__ void __launch_bounds__(kLThreads, MinBlocks<K>::v) k_leaf(LeafPK a, D
     int wpos = -0x40000000;  // far from every staged index: no window
     constexpr int NW = WinN<K>::N;
     bool staged0 = false;
-    if (!LB && a.self && a.k == K && s1o - s0o >= NW) {
+    if (!JZ_OWN_EXACT && !LB && a.self && a.k == K && s1o - s0o >= NW) {
       if (act) wpos = min(max(qi - NW / 2, s0o), s1o - NW);
       if (JZ_WIN_SMEM && s1o - s0o <= kLCap) {  // the own block fits one batch: window from smem
         const int m = s1o - s0o;
@@ -850,7 +960,10 @@ __global__ void __launch_bounds__(kLThreads, MinBlocks<K>::v) k_leaf(LeafPK a, D
     }
 #endif
     L.stg += xb - xa;
-    own_pass<K, LB, PER>(a, D, B, s0o, s1o, cls_all, wpos, qx, qy, qz, act, L, nev, staged0);
+    if (JZ_OWN_EXACT && !LB)
+      own_exact<K, LB, PER>(a, D, B, s0o, s1o, cls_all, qx, qy, qz, act, L, nev);
+    else
+      own_pass<K, LB, PER>(a, D, B, s0o, s1o, cls_all, wpos, qx, qy, qz, act, L, nev, staged0);
     if (JZ_MERGE_T > 0) merge<K, LB>(B, L);
   }
   const unsigned o_app = L.app, o_rnd = L.rnd, o_cmp = L.cmp, o_stp = L.stp, o_pst = L.pst;
