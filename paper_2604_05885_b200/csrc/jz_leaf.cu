@@ -254,14 +254,34 @@ struct Lane {
   bool act;
 };
 
+#ifndef JZ_MERGE_NET
+#define JZ_MERGE_NET 0  // > 0: merges with >= JZ_MERGE_NET new entries in some lane use the 8-value network
+#endif
+template <int K>
+__device__ __forceinline__ void net_merge8(float (&F)[K], float (&N)[8]);
+
 // merge the lane's new log entries into F (all lanes in lockstep: max(new) rounds)
 template <int K, bool LB>
 __device__ __forceinline__ void merge(WarpBuf<K> &B, Lane<K, LB> &L) {
   const int lane = threadIdx.x & 31;
   const int nr = (int)__reduce_max_sync(0xffffffffu, (unsigned)(L.nl - L.nf));
   if (JZ_STATS) L.rnd += nr;
+  int i = 0;
+#if JZ_MERGE_NET > 0
+  // many new entries in some lane: 8 at a time through the sort / bitonic-merge network
 #pragma unroll 1
-  for (int i = 0; i < nr; i += 2) {  // two entries per round
+  for (; nr - i >= JZ_MERGE_NET; i += 8) {
+    float N[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int r = L.nf + i + u;
+      N[u] = __uint_as_float(r < L.nl ? (unsigned)(B.lk[r][lane] >> 32) : 0x7f800000u);
+    }
+    net_merge8<K>(L.F, N);
+  }
+#endif
+#pragma unroll 1
+  for (; i < nr; i += 2) {  // two entries per round
     const int r = L.nf + i;
     const float d1 = __uint_as_float(r < L.nl ? (unsigned)(B.lk[r][lane] >> 32) : 0x7f800000u);
     const float d2 = __uint_as_float(r + 1 < L.nl ? (unsigned)(B.lk[r + 1][lane] >> 32) : 0x7f800000u);
@@ -755,6 +775,9 @@ __device__ __forceinline__ void own_pass(const LeafPK &a, const Dom &D, WarpBuf<
 #ifndef JZ_OWN_EXACT
 #define JZ_OWN_EXACT 1
 #endif
+#ifndef JZ_OWN_EXT
+#define JZ_OWN_EXT 0  // leaves of J added on each side of the own block (exact pass over more sources)
+#endif
 
 // F (ascending, K values) := the K smallest of F and N (8 values, no NaN)
 template <int K>
@@ -923,6 +946,10 @@ __global__ void __launch_bounds__(kLThreads, MinBlocks<K>::v) k_leaf(LeafPK a, D
         xa = min(xa, l0 + __ffs(b) - 1);
         xb = max(xb, l0 + 32 - __clz(b));
       }
+    }
+    if (JZ_OWN_EXT > 0 && JZ_OWN_EXACT && !LB) {  // widen the own block by neighbouring leaves of J
+      xa = max(LJa, xa - JZ_OWN_EXT);
+      xb = min(LJb, xb + JZ_OWN_EXT);
     }
     const int s0o = a.sbeg[xa], s1o = a.sbeg[xb];
     int wpos = -0x40000000;  // far from every staged index: no window
