@@ -72,7 +72,7 @@ enum {
 typedef struct {
   int32_t nmax0;   /* N_max^(0), leaf capacity; 0 => 80 (paper: 48, tuned for its kernels). Range 1..128 */
   int32_t coarsen; /* c, N_max^(p) = N_max^(0) c^p; 0 => 16 (paper: 8, tuned for its kernels). >= 2 */
-  int32_t ntarget; /* N_target: build plane p >= 1 iff 2N / N_max^(p) >= N_target; 0 => 300 (paper: ~1000) */
+  int32_t ntarget; /* N_target: build plane p >= 1 iff 2N / N_max^(p) >= N_target; 0 => 30 (paper: ~1000) */
   int32_t ngr;     /* NGR, top nodes per super node; 0 => 32 */
   uint32_t flags;  /* JZ_FLAG_* */
   float frame_origin[3]; /* with JZ_FLAG_FRAME: key frame origin (open boundary) */

@@ -63,7 +63,7 @@ jz_knn_params normalize(const jz_knn_params *p) {
   if (p) r = *p;
   if (r.nmax0 <= 0) r.nmax0 = 80;  // larger leaves amortise the walk (paper default 48)
   if (r.coarsen <= 0) r.coarsen = 16;   // fewer, larger plane-1 nodes (paper 8)
-  if (r.ntarget <= 0) r.ntarget = 300;  // with c = 16: 4 planes at 10^8 (paper ~1000)
+  if (r.ntarget <= 0) r.ntarget = 30;  // with c = 16: planes 1-4 at 10^8 (paper ~1000; tools/variants/g_nt.sh)
   if (r.ngr <= 0) r.ngr = 32;
   return r;
 }

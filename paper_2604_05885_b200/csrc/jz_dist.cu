@@ -180,6 +180,41 @@ __device__ __forceinline__ NodeBox qbox_at(const float *__restrict__ q, int64_t 
 }
 
 constexpr int kGhostCand = 2048;
+constexpr int kQChunk = 32;          // query boxes per culling chunk (consecutive = Morton-ordered per rank)
+constexpr int kGhostGridMin = 1024;  // CTAs of the ghost selection: the coarsest plane with >= this many nodes
+
+// one record per chunk of kQChunk consecutive query boxes: union AABB, largest radius^2, ranks
+// present (bit r); a box of the chunk can only reach a node if the chunk does (d_low^2 is monotone
+// under box inclusion, the radius is the chunk's largest)
+__global__ void k_qchunks(const float *__restrict__ qb, int64_t nqb, float4 *__restrict__ ch) {
+  const int64_t nch = (nqb + kQChunk - 1) / kQChunk;
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nch; c += (int64_t)gridDim.x * blockDim.x) {
+    float4 lo = make_float4(INFINITY, INFINITY, INFINITY, 0.f), hi = make_float4(-INFINITY, -INFINITY, -INFINITY, 0.f);
+    float r2m = 0.f;
+    unsigned rm = 0;
+    for (int64_t j = c * kQChunk; j < min(nqb, (c + 1) * kQChunk); ++j) {
+      const float4 a = reinterpret_cast<const float4 *>(qb)[2 * j];
+      const float4 b = reinterpret_cast<const float4 *>(qb)[2 * j + 1];
+      const int rk = __float_as_int(b.w);
+      if (rk < 0 || rk > 31) continue;
+      lo = make_float4(fminf(lo.x, a.x), fminf(lo.y, a.y), fminf(lo.z, a.z), 0.f);
+      hi = make_float4(fmaxf(hi.x, b.x), fmaxf(hi.y, b.y), fmaxf(hi.z, b.z), 0.f);
+      r2m = fmaxf(r2m, a.w);
+      rm |= 1u << rk;
+    }
+    lo.w = r2m;
+    hi.w = __uint_as_float(rm);
+    ch[2 * c] = lo;
+    ch[2 * c + 1] = hi;
+  }
+}
+
+// the plane whose nodes are the CTAs of k_select_ghosts (enough CTAs for the chip)
+static int ghost_grid_plane(const std::vector<Plane> &pl) {
+  for (int p = (int)pl.size() - 1; p > 0; --p)
+    if (pl[p].nnodes >= kGhostGridMin) return p;
+  return 0;
+}
 constexpr int kGhostHit = 16;  // query boxes per leaf kept for the point-level filter
 
 // one CTA per node of the top plane: candidate peer boxes (CTA-wide), then one warp per leaf:
@@ -193,7 +228,7 @@ __global__ void __launch_bounds__(256) k_select_ghosts(const float4 *__restrict_
                                                        int64_t nqb, int self, Dom D, int32_t *__restrict__ mask,
                                                        const int2 *__restrict__ box_leaves,
                                                        const float *__restrict__ leafqb, int32_t *__restrict__ hit_leaf,
-                                                       int32_t *__restrict__ cand_g) {
+                                                       int32_t *__restrict__ cand_g, const float4 *__restrict__ qch) {
   // cand_g (optional, [gridDim.x][nqb]): candidates beyond the kGhostCand kept in shared memory
   // hit_leaf (optional): receiver leaves that some sent point reaches. Query box j covers the
   // receiver's leaf boxes [box_leaves[j].x, box_leaves[j].y) of leafqb (AABB + the leaf's own
@@ -212,16 +247,25 @@ __global__ void __launch_bounds__(256) k_select_ghosts(const float4 *__restrict_
   }
   __syncthreads();
   const NodeBox tb = topbox[T];
-  for (int64_t j = threadIdx.x; j < nqb; j += blockDim.x) {
-    float r2;
-    int rk;
-    const NodeBox b = qbox_at(qb, j, &r2, &rk);
-    if (rk == self) continue;
-    if (box_dlow2(tb, b, D) <= r2) {
-      int p = atomicAdd(&s_n, 1);
-      if (p < kGhostCand) s_cand[p] = (int)j;
-      else if (cand_g) cand_g[T * nqb + p] = (int)j;
-      else s_over = 1;
+  const int64_t nch = (nqb + kQChunk - 1) / kQChunk;
+  for (int64_t c = threadIdx.x; c < nch; c += blockDim.x) {  // chunks first, then their boxes
+    const float4 clo = qch[2 * c], chi = qch[2 * c + 1];
+    if ((__float_as_uint(chi.w) & ~(1u << self)) == 0u) continue;
+    NodeBox cb;
+    cb.lo = make_float4(clo.x, clo.y, clo.z, 0.f);
+    cb.hi = make_float4(chi.x, chi.y, chi.z, 0.f);
+    if (!(box_dlow2(tb, cb, D) <= clo.w)) continue;
+    for (int64_t j = c * kQChunk; j < min(nqb, (c + 1) * kQChunk); ++j) {
+      float r2;
+      int rk;
+      const NodeBox b = qbox_at(qb, j, &r2, &rk);
+      if (rk == self) continue;
+      if (box_dlow2(tb, b, D) <= r2) {
+        int p = atomicAdd(&s_n, 1);
+        if (p < kGhostCand) s_cand[p] = (int)j;
+        else if (cand_g) cand_g[T * nqb + p] = (int)j;
+        else s_over = 1;
+      }
     }
   }
   __syncthreads();
@@ -501,13 +545,18 @@ int jz_knn_select_ghosts(jz_knn_index *ix, const float *boxes, int64_t nbox, int
     cudaStream_t st = (cudaStream_t)s;
     jz::IndexView v = jz::view_of(ix);
     const auto &pl = *v.planes;
-    const int top = (int)pl.size() - 1;
+    const int top = jz::ghost_grid_plane(pl);
     JZ_CUDA(cudaMemsetAsync(counts, 0, nranks * sizeof(int64_t), st));
     if (nbox > 0) {
+      float4 *qch = nullptr;
+      const int64_t nch = (nbox + jz::kQChunk - 1) / jz::kQChunk;
+      JZ_CUDA(cudaMallocAsync(&qch, nch * 2 * sizeof(float4), st));
+      jz::k_qchunks<<<jz::grid_for(nch, 256), 256, 0, st>>>(boxes, nbox, qch);
       jz::k_select_ghosts<<<(unsigned)pl[top].nnodes, 256, 0, st>>>(v.pts, pl[top].box, pl[top].leafspl, pl[0].box,
                                                                      pl[0].beg, boxes, nbox, self_rank, v.D, mask,
-                                                                     nullptr, nullptr, nullptr, nullptr);
+                                                                     nullptr, nullptr, nullptr, nullptr, qch);
       JZ_LAUNCH_CHECK();
+      JZ_CUDA(cudaFreeAsync(qch, st));
       jz::k_ghost_count<<<jz::grid_for(v.n, 256, 148 * 4), 256, 0, st>>>(mask, v.n, nranks,
                                                                           (unsigned long long *)counts);
       JZ_LAUNCH_CHECK();
@@ -1022,13 +1071,16 @@ int jz_knn_query_dist(jz_knn_index *ix, int k, int order, int32_t *out_idx, floa
         int32_t *mask = S.get<int32_t>(m);
         int64_t *gc = S.get<int64_t>(R);
         const auto &pl = ix->planes;
-        const int top = (int)pl.size() - 1;
+        const int top = ghost_grid_plane(pl);
         JZ_CUDA(cudaMemsetAsync(gc, 0, R * sizeof(int64_t), st));
         int32_t *cand_g = (int64_t)pl[top].nnodes * nb <= (int64_t)1 << 28 ? S.get<int32_t>(pl[top].nnodes * nb) : nullptr;
+        const int64_t nch = (nb + kQChunk - 1) / kQChunk;
+        float4 *qch = reinterpret_cast<float4 *>(S.get<float>(nch * 8));
+        k_qchunks<<<grid_for(nch, 256), 256, 0, st>>>(allb, nb, qch);
         mark("pre-select");
         k_select_ghosts<<<(unsigned)pl[top].nnodes, 256, 0, st>>>(ix->pts, pl[top].box, pl[top].leafspl, pl[0].box,
                                                                    pl[0].beg, allb, nb, r, ix->D, mask, allr, alll, hit,
-                                                                   cand_g);
+                                                                   cand_g, qch);
         JZ_LAUNCH_CHECK();
         mark("k_select_ghosts");
         if (prof) fprintf(stderr, "rank %d top nodes %lld boxes %lld leaves %lld\n", r, (long long)pl[top].nnodes, (long long)nb, (long long)nl);
