@@ -214,6 +214,9 @@ __global__ void __launch_bounds__(kN2NWarps * 32) k_n2n(const int32_t *__restric
 // ---- flat variant: one thread per receiving child (all lanes busy whatever the fan-out c); the
 // source boxes come through L1 (consecutive children share their parent's list, so a warp mostly
 // reads the same boxes). Same decisions as k_n2n, per child instead of per 32-child chunk.
+#ifndef JZ_N2N_WC
+#define JZ_N2N_WC 1  // warp per receiving child (k_n2n_wc) instead of a thread per child (k_n2n_flat)
+#endif
 #ifndef JZ_N2N_FLAT
 #define JZ_N2N_FLAT 1
 #endif
@@ -283,6 +286,97 @@ __global__ void __launch_bounds__(256) k_n2n_flat(const int32_t *__restrict__ cp
     }
     if (MODE == RMAX) rmax2[c] = R;
     if (MODE == COUNT) cnt[c] = count;
+  }
+}
+
+// ---- warp-per-child variant (JZ_N2N_WC): one warp per receiving child, lanes over the children of
+// each list entry (box loads and bounds in parallel, 32x the threads of k_n2n_flat). RMAX runs the
+// same sequential count heap as the flat kernel, every lane redundantly on the shuffled candidates in
+// list order, so R, the counts and the list order are identical (results bit-identical).
+template <int MODE>
+__global__ void __launch_bounds__(256) k_n2n_wc(const int32_t *__restrict__ cpar, int64_t nchild,
+                                                const int32_t *__restrict__ pbeg, const int64_t *__restrict__ ispl,
+                                                const int32_t *__restrict__ isrc, const float *__restrict__ rlow,
+                                                const NodeBox *__restrict__ cbox, Dom D, int k, int sorted, int early,
+                                                float *__restrict__ rmax2, int32_t *__restrict__ cnt,
+                                                const int64_t *__restrict__ ispl_out, int32_t *__restrict__ isrc_out,
+                                                float *__restrict__ rlow_out, const uint8_t *__restrict__ qf) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t c = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); c < nchild; c += nw) {
+    if (qf && !qf[c]) {
+      if (lane == 0) {
+        if (MODE == RMAX) rmax2[c] = 0.f;
+        if (MODE == COUNT) cnt[c] = 0;
+      }
+      continue;
+    }
+    const int J = cpar[c];
+    const NodeBox mb = cbox[c];
+    CountHeap h;
+    float R = INFINITY;
+    if (MODE == RMAX) {
+#pragma unroll
+      for (int j = 0; j < kHeap; ++j) {
+        h.r[j] = INFINITY;
+        h.c[j] = 0;
+      }
+      h.tot = 0;
+    } else {
+      R = rmax2[c];
+    }
+    int count = 0;
+    int64_t wp = MODE == INSERT ? ispl_out[c] : 0;
+    const int64_t eb = ispl[J], ee = ispl[J + 1];
+    for (int64_t e = eb; e < ee; ++e) {
+      const float rl = rlow[e];
+      if (early && (MODE == RMAX ? !(rl < R) : !(rl <= R))) {
+        if (sorted) break;
+        continue;
+      }
+      const int S = isrc[e];
+      const int s0 = pbeg[S], s1 = pbeg[S + 1];
+      for (int b = s0; b < s1; b += 32) {
+        const int s = b + lane;
+        const bool in = s < s1;
+        if (MODE == RMAX) {
+          float r2 = INFINITY;
+          int bc = 0;
+          if (in) {
+            const NodeBox sbx = cbox[s];
+            r2 = box_dup2(mb, sbx, D);
+            bc = box_count(sbx);
+          }
+          unsigned m = __ballot_sync(0xffffffffu, in && r2 < R);
+          while (m) {  // list order, the same test against the running radius as the flat kernel
+            const int j = __ffs(m) - 1;
+            m &= m - 1;
+            const float rj = __shfl_sync(0xffffffffu, r2, j);
+            const int cj = __shfl_sync(0xffffffffu, bc, j);
+            if (rj < R) {
+              heap_insert(h, rj, cj, k);
+              R = heap_radius(h, k);
+            }
+          }
+        } else {
+          float dl = INFINITY;
+          if (in) dl = box_dlow2(mb, cbox[s], D);
+          const bool ok = in && dl <= R;
+          const unsigned bal = __ballot_sync(0xffffffffu, ok);
+          if (MODE == INSERT && ok) {
+            const int64_t o = wp + __popc(bal & ((1u << lane) - 1u));
+            isrc_out[o] = s;
+            rlow_out[o] = dl;
+          }
+          wp += __popc(bal);
+          count += __popc(bal);
+        }
+      }
+    }
+    if (lane == 0) {
+      if (MODE == RMAX) rmax2[c] = R;
+      if (MODE == COUNT) cnt[c] = count;
+    }
   }
 }
 
@@ -400,10 +494,12 @@ void walk_to(const std::vector<Plane> &planes, const Dom &D, int k, int ngr, uns
       JZ_LAUNCH_CHECK();
     }
     const unsigned fb = (unsigned)grid_for(pl.nnodes, 256);
+    const bool wc = JZ_N2N_WC && !getenv("JZ_N2N_THREAD");
+    const unsigned wb = (unsigned)grid_for(pl.nnodes, 8, 148 * 64);  // 8 warps per CTA
     if (fixed_r2 >= 0.f) {  // fixed-radius walk (friends-of-friends): every node keeps r^2
       k_fill_f32<<<grid_for(pl.nnodes, 256), 256, 0, st>>>(rmax2, pl.nnodes, fixed_r2);
     } else if (flat) {
-      k_n2n_flat<RMAX><<<fb, 256, 0, st>>>(cpar, pl.nnodes, pbeg, il.ispl, il.isrc, il.rlow, pl.box, D, k, srt, ee, rmax2,
+      (wc ? k_n2n_wc<RMAX> : k_n2n_flat<RMAX>)<<<wc ? wb : fb, 256, 0, st>>>(cpar, pl.nnodes, pbeg, il.ispl, il.isrc, il.rlow, pl.box, D, k, srt, ee, rmax2,
                                              nullptr, nullptr, nullptr, nullptr, qf[p]);
     } else {
       k_n2n<RMAX><<<(unsigned)ceil_div(npar, kN2NWarps), kN2NWarps * 32, 0, st>>>(pbeg, npar, il.ispl, il.isrc, il.rlow,
@@ -412,7 +508,7 @@ void walk_to(const std::vector<Plane> &planes, const Dom &D, int k, int ngr, uns
     }
     JZ_LAUNCH_CHECK();
     if (flat)
-      k_n2n_flat<COUNT><<<fb, 256, 0, st>>>(cpar, pl.nnodes, pbeg, il.ispl, il.isrc, il.rlow, pl.box, D, k, srt, ee,
+      (wc ? k_n2n_wc<COUNT> : k_n2n_flat<COUNT>)<<<wc ? wb : fb, 256, 0, st>>>(cpar, pl.nnodes, pbeg, il.ispl, il.isrc, il.rlow, pl.box, D, k, srt, ee,
                                               rmax2, cnt, nullptr, nullptr, nullptr, qf[p]);
     else
       k_n2n<COUNT><<<(unsigned)ceil_div(npar, kN2NWarps), kN2NWarps * 32, 0, st>>>(pbeg, npar, il.ispl, il.isrc, il.rlow, pl.box, D, k, srt, ee,
@@ -426,7 +522,7 @@ void walk_to(const std::vector<Plane> &planes, const Dom &D, int k, int ngr, uns
     JZ_CUDA(cudaMallocAsync(&nl.isrc, (nl.total > 0 ? nl.total : 1) * sizeof(int32_t), st));
     JZ_CUDA(cudaMallocAsync(&nl.rlow, (nl.total > 0 ? nl.total : 1) * sizeof(float), st));
     if (flat)
-      k_n2n_flat<INSERT><<<fb, 256, 0, st>>>(cpar, pl.nnodes, pbeg, il.ispl, il.isrc, il.rlow, pl.box, D, k, srt, ee,
+      (wc ? k_n2n_wc<INSERT> : k_n2n_flat<INSERT>)<<<wc ? wb : fb, 256, 0, st>>>(cpar, pl.nnodes, pbeg, il.ispl, il.isrc, il.rlow, pl.box, D, k, srt, ee,
                                                rmax2, nullptr, nl.ispl, nl.isrc, nl.rlow, qf[p]);
     else
       k_n2n<INSERT><<<(unsigned)ceil_div(npar, kN2NWarps), kN2NWarps * 32, 0, st>>>(pbeg, npar, il.ispl, il.isrc, il.rlow, pl.box, D, k, srt, ee,
