@@ -536,6 +536,7 @@ struct LeafPK {
   int32_t *out_row_gidx;
   int self;    // queries == sources (self-query): enables the z-window initialisation
   unsigned long long *stats;  // counters (jz_knn_stats) or nullptr
+  unsigned long long *counter;  // JZ_PERSIST work-item counter of this launch (zeroed) or nullptr
 };
 
 // Pending batch of staged source leaves (one periodic shift class), carried across source nodes
@@ -881,13 +882,10 @@ __device__ const float *g_seed = nullptr;
 void exp_set_seed(const float *p) { cudaMemcpyToSymbol(g_seed, &p, sizeof(p)); }
 #endif
 
+// one 32-query work item (see the file header)
 template <int K, bool LB, bool PER>
-__global__ void __launch_bounds__(kLThreads, MinBlocks<K>::v) k_leaf(LeafPK a, Dom D) {
-  __shared__ __align__(16) WarpBuf<K> s_buf[kLWarps];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t item = a.item_off + (int64_t)blockIdx.x * kLWarps + warp;
-  if (item >= a.nitems) return;
-  WarpBuf<K> &B = s_buf[warp];
+__device__ __forceinline__ void leaf_item(const LeafPK &a, const Dom &D, WarpBuf<K> &B, int64_t item) {
+  const int lane = threadIdx.x & 31;
   const int J = a.item_par[item];
   const int LJa = a.par_leaf[J], LJb = a.par_leaf[J + 1];
   const int qhi = a.qbeg[LJb];
@@ -1124,6 +1122,30 @@ __global__ void __launch_bounds__(kLThreads, MinBlocks<K>::v) k_leaf(LeafPK a, D
     }
     if (act && a.out_row_gidx) a.out_row_gidx[row] = __float_as_int(qw);
   }
+}
+
+// JZ_PERSIST: one resident CTA set; each warp takes the next work item from a counter until the
+// launched range is exhausted (no CTA launch per item, same dynamic retirement as one item per CTA)
+#ifndef JZ_PERSIST
+#define JZ_PERSIST 1
+#endif
+template <int K, bool LB, bool PER>
+__global__ void __launch_bounds__(kLThreads, MinBlocks<K>::v) k_leaf(LeafPK a, Dom D) {
+  __shared__ __align__(16) WarpBuf<K> s_buf[kLWarps];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (JZ_PERSIST && a.counter) {
+    while (true) {
+      unsigned long long t = 0;
+      if (lane == 0) t = atomicAdd(a.counter, 1ull);
+      const int64_t item = a.item_off + (int64_t)__shfl_sync(0xffffffffu, t, 0);
+      if (item >= a.nitems) return;
+      leaf_item<K, LB, PER>(a, D, s_buf[warp], item);
+      __syncwarp();
+    }
+  }
+  const int64_t item = a.item_off + (int64_t)blockIdx.x * kLWarps + warp;
+  if (item >= a.nitems) return;
+  leaf_item<K, LB, PER>(a, D, s_buf[warp], item);
 }
 
 // ---------------------------------------------------------------- friends-of-friends (F4)
@@ -1439,14 +1461,31 @@ __global__ void k_item_fill(const int32_t *__restrict__ par_leaf, const int32_t 
   }
 }
 
+// persistent launches: as many CTAs as can be resident (occupancy x SMs), capped by the items
+template <int K, bool LB, bool PER>
+static void launch_kl(const LeafPK &la, const Dom &D, unsigned blocks, cudaStream_t st) {
+  if (la.counter) {
+    static int resident = 0;  // per instantiation
+    if (resident == 0) {
+      int nb = 0, dev = 0, sms = 0;
+      JZ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_leaf<K, LB, PER>, kLThreads, 0));
+      JZ_CUDA(cudaGetDevice(&dev));
+      JZ_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      resident = nb * sms > 0 ? nb * sms : 1;
+    }
+    if (blocks > (unsigned)resident) blocks = (unsigned)resident;
+  }
+  k_leaf<K, LB, PER><<<blocks, kLThreads, 0, st>>>(la, D);
+}
+
 template <int K>
 static void launch_l(const LeafPK &la, const Dom &D, unsigned blocks, cudaStream_t st) {
   if (la.col0 > 0) {  // later pass of a k > k_max query
-    if (D.periodic) k_leaf<K, true, true><<<blocks, kLThreads, 0, st>>>(la, D);
-    else k_leaf<K, true, false><<<blocks, kLThreads, 0, st>>>(la, D);
+    if (D.periodic) launch_kl<K, true, true>(la, D, blocks, st);
+    else launch_kl<K, true, false>(la, D, blocks, st);
   } else {
-    if (D.periodic) k_leaf<K, false, true><<<blocks, kLThreads, 0, st>>>(la, D);
-    else k_leaf<K, false, false><<<blocks, kLThreads, 0, st>>>(la, D);
+    if (D.periodic) launch_kl<K, false, true>(la, D, blocks, st);
+    else launch_kl<K, false, false>(la, D, blocks, st);
   }
 }
 
@@ -1504,6 +1543,8 @@ void leaf_to_leaf(const LeafArgs &a, const Dom &D, cudaStream_t st) {
   la.out_row_gidx = a.out_row_gidx;
   la.stats = a.evals;
   la.self = a.spts == a.qpts;
+  la.counter = nullptr;
+  unsigned long long *counters = nullptr;
   if (nitems > 0) {
     // chunked launches (a.on_rows: rows of the finished z-order query range after each chunk,
     // e.g. to stream them to the host while the next chunk runs); k <= k_max only
@@ -1513,6 +1554,11 @@ void leaf_to_leaf(const LeafArgs &a, const Dom &D, cudaStream_t st) {
       q0h.resize(nitems);
       JZ_CUDA(cudaMemcpyAsync(q0h.data(), item_q0, nitems * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
       JZ_CUDA(cudaStreamSynchronize(st));
+    }
+    const int npass = (a.k + kMaxK - 1) / kMaxK;
+    if (JZ_PERSIST) {  // one zeroed work-item counter per launch
+      JZ_CUDA(cudaMallocAsync(&counters, (size_t)nch * npass * sizeof(unsigned long long), st));
+      JZ_CUDA(cudaMemsetAsync(counters, 0, (size_t)nch * npass * sizeof(unsigned long long), st));
     }
     for (int ch = 0; ch < nch; ++ch) {
       const int64_t i0 = nitems * ch / nch, i1 = nitems * (ch + 1) / nch;
@@ -1525,6 +1571,7 @@ void leaf_to_leaf(const LeafArgs &a, const Dom &D, cudaStream_t st) {
       for (int c0 = 0; c0 < a.k; c0 += kMaxK) {
         la.col0 = c0;
         la.k = a.k - c0 < kMaxK ? a.k - c0 : kMaxK;
+        if (counters) la.counter = counters + (size_t)ch * npass + c0 / kMaxK;
         if (la.k <= 8) launch_l<8>(la, D, blocks, st);
         else if (la.k <= 16) launch_l<16>(la, D, blocks, st);
         else launch_l<32>(la, D, blocks, st);
@@ -1533,6 +1580,7 @@ void leaf_to_leaf(const LeafArgs &a, const Dom &D, cudaStream_t st) {
       if (nch > 1) a.on_rows(q0h[i0], i1 < nitems ? (int64_t)q0h[i1] : a.nq);
     }
   }
+  if (counters) JZ_CUDA(cudaFreeAsync(counters, st));
   JZ_CUDA(cudaFreeAsync(cnt, st));
   JZ_CUDA(cudaFreeAsync(off, st));
   JZ_CUDA(cudaFreeAsync(item_par, st));
