@@ -181,7 +181,10 @@ __device__ __forceinline__ NodeBox qbox_at(const float *__restrict__ q, int64_t 
 
 constexpr int kGhostCand = 2048;
 constexpr int kQChunk = 32;          // query boxes per culling chunk (consecutive = Morton-ordered per rank)
-constexpr int kGhostGridMin = 1024;  // CTAs of the ghost selection: the coarsest plane with >= this many nodes
+#ifndef JZ_GHOST_GRID_MIN
+#define JZ_GHOST_GRID_MIN 8192
+#endif
+constexpr int kGhostGridMin = JZ_GHOST_GRID_MIN;  // CTAs of the ghost selection: the coarsest plane with >= this many nodes
 
 // one record per chunk of kQChunk consecutive query boxes: union AABB, largest radius^2, ranks
 // present (bit r); a box of the chunk can only reach a node if the chunk does (d_low^2 is monotone
