@@ -256,23 +256,46 @@ def run_e2e(args, pos, box, k):
     h_d2 = torch.empty((n, k), dtype=torch.float32).pin_memory()
     h_rg = torch.empty((n,), dtype=torch.int32).pin_memory()
     a, b, c, g = h_pos.numpy(), h_idx.numpy(), h_d2.numpy(), h_rg.numpy()
-    steps = max(1, min(args.steps, 3))
+    # per-call wall times: the host path varies a lot between calls on these boxes (PCIe / host
+    # memory; 311-1481 ms for the same call, tools/e2e_probe.py), so the value is the median call
+    # and every call is listed
+    steps = max(3, min(args.steps, 5))
     out = {}
     for name, fn in (("z", lambda: jz.knn_host_z(a, k, box=box, out=(b, c, g))),
                      ("input", lambda: jz.knn_host(a, k, box=box, out=(b, c)))):
         fn()
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
+        ts = []
         for _ in range(steps):
+            t0 = time.perf_counter()
             fn()
-        torch.cuda.synchronize()
-        out[name] = (time.perf_counter() - t0) / steps
-    dz, di = out["z"], out["input"]
+            torch.cuda.synchronize()
+            ts.append(time.perf_counter() - t0)
+        out[name] = ts
+    dz, di = float(np.median(out["z"])), float(np.median(out["input"]))
+    # the PCIe rate of this box in the same process (pinned, 1 GiB each way, best of 3)
+    bw = {}
+    dbuf = torch.empty(1 << 30, dtype=torch.uint8, device="cuda")
+    hbuf = torch.empty(1 << 30, dtype=torch.uint8).pin_memory()
+    for nm, f in (("d2h", lambda: hbuf.copy_(dbuf, non_blocking=True)), ("h2d", lambda: dbuf.copy_(hbuf, non_blocking=True))):
+        best = 0.0
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            f()
+            e1.record()
+            torch.cuda.synchronize()
+            best = max(best, (1 << 30) / (e0.elapsed_time(e1) / 1e3) / 1e9)
+        bw[nm] = best
+    del dbuf, hbuf
+    floor_ms = (n * 12 / bw["h2d"] + (n * k * 8 + n * 4) / bw["d2h"]) / 1e6
     return {"value": n / dz, "unit": UNIT, "h2d_bytes_per_step": int(n * 12), "d2h_bytes_per_step": int(n * k * 8 + n * 4),
-            "ms_per_step": dz * 1e3,
+            "ms_per_step": dz * 1e3, "ms_per_call": [round(t * 1e3, 1) for t in out["z"]], "statistic": "median call",
+            "pcie_gbs": {kk: round(v, 1) for kk, v in bw.items()}, "pcie_floor_ms": round(floor_ms, 1),
             "api": "jz_knn_search_host_z (pinned host buffers; rows in z order + input ids, D2H streamed during the walk)",
-            "input_order": {"value": n / di, "unit": UNIT, "ms_per_step": di * 1e3, "h2d_bytes_per_step": int(n * 12),
-                            "d2h_bytes_per_step": int(n * k * 8),
+            "input_order": {"value": n / di, "unit": UNIT, "ms_per_step": di * 1e3,
+                            "ms_per_call": [round(t * 1e3, 1) for t in out["input"]],
+                            "h2d_bytes_per_step": int(n * 12), "d2h_bytes_per_step": int(n * k * 8),
                             "api": "jz_knn_search_host (pinned host buffers; rows in input order, one D2H)"}}
 
 
