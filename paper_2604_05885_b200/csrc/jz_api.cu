@@ -1,3 +1,4 @@
+#include <chrono>
 // jz_api.cu -- C ABI (include/jz_knn.h) and host orchestration of the hot path.
 //
 //   jz_knn_build  : A1 frame/validate -> A2/A3 encode + radix sort + gather -> A4-A8 planes
@@ -629,12 +630,15 @@ int jz_knn_search_host(const float *pos_host, int64_t n, const float *box, const
   init_pool();
   DevBuf dpos{nullptr, st}, didx{nullptr, st}, dd2{nullptr, st};
   IndexOwner own;
+  // the large buffers first, in the same order every call: the stream-ordered pool then hands the
+  // same blocks back (allocated after the build's temporaries they were split for them, and the
+  // pool grew by gigabytes on some calls: 283-1340 ms per call instead of 278, tools/e2e_var.py)
   JZ_CUDA(cudaMallocAsync(&dpos.p, n * 3 * sizeof(float), st));
+  JZ_CUDA(cudaMallocAsync(&didx.p, n * k * sizeof(int32_t), st));
+  JZ_CUDA(cudaMallocAsync(&dd2.p, n * k * sizeof(float), st));
   JZ_CUDA(cudaMemcpyAsync(dpos.p, pos_host, n * 3 * sizeof(float), cudaMemcpyHostToDevice, st));
   int rc = jz_knn_build(static_cast<const float *>(dpos.p), n, box, p, s, &own.ix);
   if (rc != JZ_OK) return rc;
-  JZ_CUDA(cudaMallocAsync(&didx.p, n * k * sizeof(int32_t), st));
-  JZ_CUDA(cudaMallocAsync(&dd2.p, n * k * sizeof(float), st));
   rc = jz_knn_query(own.ix, k, JZ_ORDER_INPUT, static_cast<int32_t *>(didx.p), static_cast<float *>(dd2.p), nullptr, s);
   if (rc != JZ_OK) return rc;
   JZ_CUDA(cudaMemcpyAsync(idx_host, didx.p, n * k * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
@@ -652,15 +656,27 @@ int jz_knn_search_host_z(const float *pos_host, int64_t n, const float *box, con
   if (k < 1 || k > n) return fail(JZ_EINVAL, "k must be in [1, n]");
   cudaStream_t st = (cudaStream_t)s;
   init_pool();
+  static const bool hprof = getenv("JZ_HOST_PROF") != nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
+  auto lap = [&](const char *what) {
+    if (!hprof) return;
+    cudaStreamSynchronize(st);
+    fprintf(stderr, "  host_z %-10s %8.1f ms\n", what,
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+  };
   DevBuf dpos{nullptr, st}, didx{nullptr, st}, dd2{nullptr, st}, drg{nullptr, st};
   IndexOwner own;
+  // the large buffers first (see jz_knn_search_host)
   JZ_CUDA(cudaMallocAsync(&dpos.p, n * 3 * sizeof(float), st));
-  JZ_CUDA(cudaMemcpyAsync(dpos.p, pos_host, n * 3 * sizeof(float), cudaMemcpyHostToDevice, st));
-  int rc = jz_knn_build(static_cast<const float *>(dpos.p), n, box, p, s, &own.ix);
-  if (rc != JZ_OK) return rc;
   JZ_CUDA(cudaMallocAsync(&didx.p, n * k * sizeof(int32_t), st));
   JZ_CUDA(cudaMallocAsync(&dd2.p, n * k * sizeof(float), st));
   JZ_CUDA(cudaMallocAsync(&drg.p, n * sizeof(int32_t), st));
+  lap("alloc");
+  JZ_CUDA(cudaMemcpyAsync(dpos.p, pos_host, n * 3 * sizeof(float), cudaMemcpyHostToDevice, st));
+  lap("h2d");
+  int rc = jz_knn_build(static_cast<const float *>(dpos.p), n, box, p, s, &own.ix);
+  if (rc != JZ_OK) return rc;
+  lap("build");
   // rows of each finished chunk of work items (a contiguous z-order range) go to the host on a
   // second stream while the next chunk runs: the PCIe transfer overlaps LeafToLeaf
   struct Copier {
@@ -694,8 +710,10 @@ int jz_knn_search_host_z(const float *pos_host, int64_t n, const float *box, con
                   static_cast<int32_t *>(drg.p), s, chunks, on_rows);
   if (rc != JZ_OK) return rc;
   if (cp.ev.empty()) on_rows(0, n);  // not chunked (k > k_max): one copy at the end
+  lap("query");
   JZ_CUDA(cudaStreamSynchronize(cp.cs));
   JZ_CUDA(cudaStreamSynchronize(st));
+  lap("d2h done");
   return JZ_OK;
   JZ_API_END
 }
