@@ -63,13 +63,40 @@ __device__ __forceinline__ unsigned long long warp_slot(unsigned long long *curs
   return base + (unsigned long long)__popc(peers & ((1u << lane) - 1u));
 }
 
-__global__ void k_pack(const float *__restrict__ pos, int64_t n, int64_t gbase, const int32_t *__restrict__ dest,
-                       const int64_t *__restrict__ off, unsigned long long *__restrict__ cursor,
-                       float4 *__restrict__ out) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int r = dest[i];
-    const unsigned long long p = warp_slot(cursor, r);
-    out[off[r] + (int64_t)p] = make_float4(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2], __int_as_float((int)(gbase + i)));
+// slots per destination rank aggregated per CTA (1024 points per round: shared-memory counters,
+// then one global atomic per rank and round; per-warp atomics on the R cursors serialised: 0.6 ms
+// per rank at 1.25e7 points). The order inside a destination is arbitrary (the receiver sorts).
+constexpr int kPackThreads = 256, kPackIPT = 4;
+__global__ void __launch_bounds__(kPackThreads) k_pack(const float *__restrict__ pos, int64_t n, int64_t gbase,
+                                                       const int32_t *__restrict__ dest,
+                                                       const int64_t *__restrict__ off,
+                                                       unsigned long long *__restrict__ cursor, float4 *__restrict__ out) {
+  __shared__ unsigned s_cnt[32];
+  __shared__ unsigned long long s_base[32];
+  constexpr int T = kPackThreads * kPackIPT;
+  for (int64_t b = (int64_t)blockIdx.x * T; b < n; b += (int64_t)gridDim.x * T) {
+    if (threadIdx.x < 32) s_cnt[threadIdx.x] = 0;
+    __syncthreads();
+    int r[kPackIPT];
+    unsigned loc[kPackIPT];
+#pragma unroll
+    for (int u = 0; u < kPackIPT; ++u) {
+      const int64_t i = b + u * kPackThreads + threadIdx.x;
+      r[u] = i < n ? dest[i] : -1;
+      loc[u] = r[u] >= 0 ? atomicAdd(&s_cnt[r[u]], 1u) : 0u;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32 && s_cnt[threadIdx.x] > 0)
+      s_base[threadIdx.x] = atomicAdd(&cursor[threadIdx.x], (unsigned long long)s_cnt[threadIdx.x]);
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < kPackIPT; ++u) {
+      const int64_t i = b + u * kPackThreads + threadIdx.x;
+      if (r[u] >= 0)
+        out[off[r[u]] + (int64_t)(s_base[r[u]] + loc[u])] =
+            make_float4(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2], __int_as_float((int)(gbase + i)));
+    }
+    __syncthreads();
   }
 }
 
@@ -427,7 +454,7 @@ int jz_pack_by_rank(const float *pos, int64_t n, int64_t gidx_base, const int32_
     JZ_CUDA(cudaMallocAsync(&cur, nranks * sizeof(unsigned long long), st));
     JZ_CUDA(cudaMemsetAsync(cur, 0, nranks * sizeof(unsigned long long), st));
     if (n > 0) {
-      jz::k_pack<<<jz::grid_for(n, 256), 256, 0, st>>>(pos, n, gidx_base, dest, offsets, cur, (float4 *)out4);
+      jz::k_pack<<<jz::grid_for(n, jz::kPackThreads * jz::kPackIPT), jz::kPackThreads, 0, st>>>(pos, n, gidx_base, dest, offsets, cur, (float4 *)out4);
       JZ_LAUNCH_CHECK();
     }
     JZ_CUDA(cudaFreeAsync(cur, st));
