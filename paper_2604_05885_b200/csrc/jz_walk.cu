@@ -217,6 +217,9 @@ __global__ void __launch_bounds__(kN2NWarps * 32) k_n2n(const int32_t *__restric
 #ifndef JZ_N2N_WC
 #define JZ_N2N_WC 1  // warp per receiving child (k_n2n_wc) instead of a thread per child (k_n2n_flat)
 #endif
+#ifndef JZ_N2N_WC_MAX
+#define JZ_N2N_WC_MAX (1 << 19)  // planes with at least this many children: a thread per child
+#endif
 #ifndef JZ_N2N_FLAT
 #define JZ_N2N_FLAT 1
 #endif
@@ -494,7 +497,10 @@ void walk_to(const std::vector<Plane> &planes, const Dom &D, int k, int ngr, uns
       JZ_LAUNCH_CHECK();
     }
     const unsigned fb = (unsigned)grid_for(pl.nnodes, 256);
-    const bool wc = JZ_N2N_WC && !getenv("JZ_N2N_THREAD");
+    // warp per child while the plane is small enough that a thread per child leaves the chip idle
+    // (10^8 C4 plane 1: 1.4e5 children, 7.4 -> 4.7 ms); the 2^30 C5 plane 1 (1.7e6 children) is
+    // faster with a thread per child (20.6 vs 32.9 ms)
+    const bool wc = JZ_N2N_WC && !getenv("JZ_N2N_THREAD") && pl.nnodes < JZ_N2N_WC_MAX;
     const unsigned wb = (unsigned)grid_for(pl.nnodes, 8, 148 * 64);  // 8 warps per CTA
     if (fixed_r2 >= 0.f) {  // fixed-radius walk (friends-of-friends): every node keeps r^2
       k_fill_f32<<<grid_for(pl.nnodes, 256), 256, 0, st>>>(rmax2, pl.nnodes, fixed_r2);
