@@ -1207,6 +1207,7 @@ struct FofPK {
   int sorted;
   int32_t *par;
   unsigned long long *stats;  // [0] distance evaluations
+  unsigned long long *counter;  // JZ_PERSIST work-item counter (zeroed) or nullptr
 };
 
 // staged sources [0, n) (n multiple of 8) against the lane's query qi
@@ -1263,12 +1264,8 @@ __device__ __forceinline__ int fof_pad8(FofBuf &B, int n) {
 }
 
 template <bool PER>
-__global__ void __launch_bounds__(kLThreads, 12) k_fof_leaf(FofPK a, Dom D) {
-  __shared__ __align__(16) FofBuf s_buf[kLWarps];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t item = (int64_t)blockIdx.x * kLWarps + warp;
-  if (item >= a.nitems) return;
-  FofBuf &B = s_buf[warp];
+__device__ __forceinline__ void fof_item(const FofPK &a, const Dom &D, FofBuf &B, int64_t item) {
+  const int lane = threadIdx.x & 31;
   const int J = a.item_par[item];
   const int LJa = a.par_leaf[J], LJb = a.par_leaf[J + 1];
   const int qhi = a.sbeg[LJb];
@@ -1437,6 +1434,26 @@ __global__ void __launch_bounds__(kLThreads, 12) k_fof_leaf(FofPK a, Dom D) {
     for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
     if (lane == 0) atomicAdd(&a.stats[0], tot);
   }
+}
+
+// persistent like k_leaf (JZ_PERSIST): resident CTAs take 32-query items from a counter
+template <bool PER>
+__global__ void __launch_bounds__(kLThreads, 12) k_fof_leaf(FofPK a, Dom D) {
+  __shared__ __align__(16) FofBuf s_buf[kLWarps];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (JZ_PERSIST && a.counter) {
+    while (true) {
+      unsigned long long t = 0;
+      if (lane == 0) t = atomicAdd(a.counter, 1ull);
+      const int64_t item = (int64_t)__shfl_sync(0xffffffffu, t, 0);
+      if (item >= a.nitems) return;
+      fof_item<PER>(a, D, s_buf[warp], item);
+      __syncwarp();
+    }
+  }
+  const int64_t item = (int64_t)blockIdx.x * kLWarps + warp;
+  if (item >= a.nitems) return;
+  fof_item<PER>(a, D, s_buf[warp], item);
 }
 
 // work items: 32-query groups of each receiving parent, in z order
@@ -1645,8 +1662,21 @@ void fof_leaf(const LeafArgs &a, const Dom &D, float b2, int32_t *par, cudaStrea
   f.sorted = !(a.flags & (JZ_FLAG_NO_SEGSORT | JZ_FLAG_NO_EARLY_EXIT));
   f.par = par;
   f.stats = a.evals;
+  f.counter = nullptr;
+  unsigned long long *fcnt = nullptr;
   if (nitems > 0) {
-    const unsigned blocks = (unsigned)ceil_div(nitems, kLWarps);
+    unsigned blocks = (unsigned)ceil_div(nitems, kLWarps);
+    if (JZ_PERSIST) {
+      JZ_CUDA(cudaMallocAsync(&fcnt, sizeof(unsigned long long), st));
+      JZ_CUDA(cudaMemsetAsync(fcnt, 0, sizeof(unsigned long long), st));
+      f.counter = fcnt;
+      int nb = 0, dev = 0, sms = 0;
+      if (D.periodic) JZ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_fof_leaf<true>, kLThreads, 0));
+      else JZ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_fof_leaf<false>, kLThreads, 0));
+      JZ_CUDA(cudaGetDevice(&dev));
+      JZ_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      if (nb * sms > 0 && blocks > (unsigned)(nb * sms)) blocks = (unsigned)(nb * sms);
+    }
     if (D.periodic) k_fof_leaf<true><<<blocks, kLThreads, 0, st>>>(f, D);
     else k_fof_leaf<false><<<blocks, kLThreads, 0, st>>>(f, D);
     JZ_LAUNCH_CHECK();
@@ -1657,6 +1687,7 @@ void fof_leaf(const LeafArgs &a, const Dom &D, float b2, int32_t *par, cudaStrea
   JZ_CUDA(cudaFreeAsync(item_q0, st));
   JZ_CUDA(cudaFreeAsync(leaf_ce, st));
   if (par_ce) JZ_CUDA(cudaFreeAsync(par_ce, st));
+  if (fcnt) JZ_CUDA(cudaFreeAsync(fcnt, st));
 }
 
 }  // namespace jz
