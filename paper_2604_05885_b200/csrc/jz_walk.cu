@@ -710,6 +710,65 @@ __global__ void __launch_bounds__(kN2NWarps * 32) k_fof_n2n(const int32_t *__res
   }
 }
 
+// the same three cases with one warp per receiving child and lanes over the children of each
+// list entry (as k_n2n_wc): many more threads on the coarse planes; unions are concurrent-safe
+// (CAS) and the written lists keep the (entry, child) order
+template <int MODE, bool LINKS>
+__global__ void __launch_bounds__(256) k_fof_wc(const int32_t *__restrict__ cpar, int64_t nchild,
+                                                const int32_t *__restrict__ pbeg, const int64_t *__restrict__ ispl,
+                                                const int32_t *__restrict__ isrc, const NodeBox *__restrict__ cbox,
+                                                Dom D, float b2, int32_t *__restrict__ g, uint8_t *__restrict__ lk,
+                                                int32_t *__restrict__ cnt, const int64_t *__restrict__ ispl_out,
+                                                int32_t *__restrict__ isrc_out, float *__restrict__ rlow_out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t c = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); c < nchild; c += nw) {
+    const int J = cpar[c];
+    const NodeBox mb = cbox[c];
+    const int rc = MODE != FLINK ? g[c] : 0;
+    const bool lc = MODE != FLINK ? lk[c] != 0 : false;
+    int count = 0;
+    int64_t wp = MODE == FINSERT ? ispl_out[c] : 0;
+    const int64_t eb = ispl[J], ee = ispl[J + 1];
+    for (int64_t e = eb; e < ee; ++e) {
+      const int S = isrc[e];
+      const int s1 = pbeg[S + 1];
+      for (int b = pbeg[S]; b < s1; b += 32) {
+        const int s = b + lane;
+        bool ok = false;
+        float dl = 0.f;
+        if (s < s1) {
+          const NodeBox sbx = cbox[s];
+          dl = box_dlow2(mb, sbx, D);
+          if (dl <= b2) {                                            // else case (1): too far
+            const bool full = LINKS && box_dup2(mb, sbx, D) <= b2;  // case (2): every pair within R_link
+            if (MODE == FLINK) {
+              if (full && s != (int)c) {
+                gunion(g, (int)c, s);
+                lk[c] = 1;
+                lk[s] = 1;
+              }
+            } else {
+              ok = !full && !(LINKS && lc && g[s] == rc);  // case (1): same linked group
+            }
+          }
+        }
+        if (MODE != FLINK) {
+          const unsigned bal = __ballot_sync(0xffffffffu, ok);
+          if (MODE == FINSERT && ok) {
+            const int64_t o = wp + __popc(bal & ((1u << lane) - 1u));
+            isrc_out[o] = s;
+            rlow_out[o] = dl;
+          }
+          wp += __popc(bal);
+          count += __popc(bal);
+        }
+      }
+    }
+    if (MODE == FCOUNT && lane == 0) cnt[c] = count;
+  }
+}
+
 __global__ void k_fof_point_init(const int32_t *__restrict__ beg, int64_t nleaf, const int32_t *__restrict__ g,
                                  const uint8_t *__restrict__ lk, int32_t *__restrict__ par) {
   for (int64_t l = blockIdx.x; l < nleaf; l += gridDim.x) {
@@ -782,7 +841,21 @@ void fof_walk(const std::vector<Plane> &planes, const Dom &D, int ngr, float b2,
     float mdq;
     memcpy(&mdq, &mh, 4);
     const bool links = mdq <= b2;
-    if (links) {
+    const bool fwc = JZ_N2N_WC && !getenv("JZ_N2N_THREAD") && pl.nnodes < JZ_N2N_WC_MAX;
+    int32_t *cpar = nullptr;
+    const unsigned wb = (unsigned)grid_for(pl.nnodes, 8, 148 * 64);
+    if (fwc) {
+      JZ_CUDA(cudaMallocAsync(&cpar, (pl.nnodes > 0 ? pl.nnodes : 1) * sizeof(int32_t), st));
+      k_child_parent<<<grid_for(npar, 256), 256, 0, st>>>(pbeg, npar, cpar);
+      JZ_LAUNCH_CHECK();
+    }
+    if (links && fwc) {
+      k_fof_wc<FLINK, true><<<wb, 256, 0, st>>>(cpar, pl.nnodes, pbeg, il.ispl, il.isrc, pl.box, D, b2, g, lk, nullptr,
+                                                nullptr, nullptr, nullptr);
+      JZ_LAUNCH_CHECK();
+      k_fof_contract<<<grid_for(pl.nnodes, 256), 256, 0, st>>>(g, pl.nnodes);
+      JZ_LAUNCH_CHECK();
+    } else if (links) {
       k_fof_n2n<FLINK, true><<<blocks, kN2NWarps * 32, 0, st>>>(pbeg, npar, il.ispl, il.isrc, pl.box, D, b2, g, lk,
                                                                  nullptr, nullptr, nullptr, nullptr);
       JZ_LAUNCH_CHECK();
@@ -791,7 +864,13 @@ void fof_walk(const std::vector<Plane> &planes, const Dom &D, int ngr, float b2,
     }
     int32_t *cnt = nullptr;
     JZ_CUDA(cudaMallocAsync(&cnt, pl.nnodes * sizeof(int32_t), st));
-    if (links)
+    if (fwc && links)
+      k_fof_wc<FCOUNT, true><<<wb, 256, 0, st>>>(cpar, pl.nnodes, pbeg, il.ispl, il.isrc, pl.box, D, b2, g, lk, cnt,
+                                                 nullptr, nullptr, nullptr);
+    else if (fwc)
+      k_fof_wc<FCOUNT, false><<<wb, 256, 0, st>>>(cpar, pl.nnodes, pbeg, il.ispl, il.isrc, pl.box, D, b2, g, lk, cnt,
+                                                  nullptr, nullptr, nullptr);
+    else if (links)
       k_fof_n2n<FCOUNT, true><<<blocks, kN2NWarps * 32, 0, st>>>(pbeg, npar, il.ispl, il.isrc, pl.box, D, b2, g, lk, cnt,
                                                                   nullptr, nullptr, nullptr);
     else
@@ -805,13 +884,20 @@ void fof_walk(const std::vector<Plane> &planes, const Dom &D, int ngr, float b2,
     nl.total = read_i64(nl.ispl + pl.nnodes, st);
     JZ_CUDA(cudaMallocAsync(&nl.isrc, (nl.total > 0 ? nl.total : 1) * sizeof(int32_t), st));
     JZ_CUDA(cudaMallocAsync(&nl.rlow, (nl.total > 0 ? nl.total : 1) * sizeof(float), st));
-    if (links)
+    if (fwc && links)
+      k_fof_wc<FINSERT, true><<<wb, 256, 0, st>>>(cpar, pl.nnodes, pbeg, il.ispl, il.isrc, pl.box, D, b2, g, lk,
+                                                  nullptr, nl.ispl, nl.isrc, nl.rlow);
+    else if (fwc)
+      k_fof_wc<FINSERT, false><<<wb, 256, 0, st>>>(cpar, pl.nnodes, pbeg, il.ispl, il.isrc, pl.box, D, b2, g, lk,
+                                                   nullptr, nl.ispl, nl.isrc, nl.rlow);
+    else if (links)
       k_fof_n2n<FINSERT, true><<<blocks, kN2NWarps * 32, 0, st>>>(pbeg, npar, il.ispl, il.isrc, pl.box, D, b2, g, lk,
                                                                    nullptr, nl.ispl, nl.isrc, nl.rlow);
     else
       k_fof_n2n<FINSERT, false><<<blocks, kN2NWarps * 32, 0, st>>>(pbeg, npar, il.ispl, il.isrc, pl.box, D, b2, g, lk,
                                                                     nullptr, nl.ispl, nl.isrc, nl.rlow);
     JZ_LAUNCH_CHECK();
+    if (cpar) JZ_CUDA(cudaFreeAsync(cpar, st));
     // segments in (d_low, source) order, as the kNN walk: nearby source nodes first
     k_segsort<<<grid_for(pl.nnodes, kSegWarps, 148 * 16), kSegWarps * 32, 0, st>>>(nl.ispl, nl.nrecv, nl.isrc, nl.rlow);
     JZ_LAUNCH_CHECK();
