@@ -884,7 +884,8 @@ void exp_set_seed(const float *p) { cudaMemcpyToSymbol(g_seed, &p, sizeof(p)); }
 
 // one 32-query work item (see the file header)
 template <int K, bool LB, bool PER>
-__device__ __forceinline__ void leaf_item(const LeafPK &a, const Dom &D, WarpBuf<K> &B, int64_t item) {
+__device__ __forceinline__ void leaf_item(const LeafPK &a, const Dom &D, WarpBuf<K> &B, int64_t item,
+                                          unsigned long long &acc_ev) {
   const int lane = threadIdx.x & 31;
   const int J = a.item_par[item];
   const int LJa = a.par_leaf[J], LJb = a.par_leaf[J + 1];
@@ -1033,7 +1034,12 @@ __device__ __forceinline__ void leaf_item(const LeafPK &a, const Dom &D, WarpBuf
   // the row: the k smallest keys of the log (all entries <= the final k-th value)
   compact<K, LB>(B, L);
   if (L.nl > a.k) L.nl = drop_largest<K>(B, L.nl, a.k);
-  if (a.stats) {
+  if (a.stats && !JZ_STATS) {  // evaluations only, summed per warp over its items (one atomic per warp)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nev += __shfl_xor_sync(0xffffffffu, nev, o);
+    acc_ev += nev;
+  }
+  if (a.stats && JZ_STATS) {
     unsigned long long tot = nev, ins = L.ins, app = L.app;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -1133,19 +1139,27 @@ template <int K, bool LB, bool PER>
 __global__ void __launch_bounds__(kLThreads, MinBlocks<K>::v) k_leaf(LeafPK a, Dom D) {
   __shared__ __align__(16) WarpBuf<K> s_buf[kLWarps];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned long long acc_ev = 0, acc_it = 0;  // evaluations / items of this warp (stats, non-JZ_STATS builds)
   if (JZ_PERSIST && a.counter) {
     while (true) {
       unsigned long long t = 0;
       if (lane == 0) t = atomicAdd(a.counter, 1ull);
       const int64_t item = a.item_off + (int64_t)__shfl_sync(0xffffffffu, t, 0);
-      if (item >= a.nitems) return;
-      leaf_item<K, LB, PER>(a, D, s_buf[warp], item);
+      if (item >= a.nitems) break;
+      leaf_item<K, LB, PER>(a, D, s_buf[warp], item, acc_ev);
+      ++acc_it;
       __syncwarp();
     }
+  } else {
+    const int64_t item = a.item_off + (int64_t)blockIdx.x * kLWarps + warp;
+    if (item >= a.nitems) return;
+    leaf_item<K, LB, PER>(a, D, s_buf[warp], item, acc_ev);
+    acc_it = 1;
   }
-  const int64_t item = a.item_off + (int64_t)blockIdx.x * kLWarps + warp;
-  if (item >= a.nitems) return;
-  leaf_item<K, LB, PER>(a, D, s_buf[warp], item);
+  if (!JZ_STATS && a.stats && lane == 0 && acc_it) {
+    atomicAdd(&a.stats[0], acc_ev);
+    atomicAdd(&a.stats[6], acc_it);
+  }
 }
 
 // ---------------------------------------------------------------- friends-of-friends (F4)
